@@ -1,0 +1,152 @@
+// Shared device helpers for the PolarQuant B200 kernels (sm_100a only).
+//
+// Nothing here is PolarQuant-specific: element loads for the three key dtypes,
+// mbarrier / cp.async.bulk (TMA bulk-copy engine) wrappers, warp reductions.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "../../include/pqb200.h"
+
+#define PQB_DEV __device__ __forceinline__
+
+namespace pqb {
+
+constexpr int kWarp = 32;
+
+// ----------------------------------------------------------------- dtypes
+
+template <int DT> struct DType;
+template <> struct DType<PQB_F32>  { using T = float;          static constexpr int kBytes = 4; };
+template <> struct DType<PQB_BF16> { using T = __nv_bfloat16;  static constexpr int kBytes = 2; };
+template <> struct DType<PQB_F16>  { using T = __half;         static constexpr int kBytes = 2; };
+
+PQB_DEV float to_f32(float v) { return v; }
+PQB_DEV float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+PQB_DEV float to_f32(__half v) { return __half2float(v); }
+
+// Load 8 consecutive elements (16-byte aligned for 2-byte types, 32-byte for f32)
+// and widen to f32.  Widening is exact for every supported dtype.
+template <int DT>
+PQB_DEV void load8(const void* base, int64_t elem_off, float (&out)[8]) {
+  if constexpr (DT == PQB_F32) {
+    const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(base) + elem_off);
+    float4 a = __ldg(p), b = __ldg(p + 1);
+    out[0] = a.x; out[1] = a.y; out[2] = a.z; out[3] = a.w;
+    out[4] = b.x; out[5] = b.y; out[6] = b.z; out[7] = b.w;
+  } else {
+    const uint4* p = reinterpret_cast<const uint4*>(
+        static_cast<const typename DType<DT>::T*>(base) + elem_off);
+    uint4 w = __ldg(p);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if constexpr (DT == PQB_BF16) {
+        out[2 * i] = __uint_as_float(ws[i] << 16);
+        out[2 * i + 1] = __uint_as_float(ws[i] & 0xffff0000u);
+      } else {
+        __half2 h = *reinterpret_cast<const __half2*>(&ws[i]);
+        float2 f = __half22float2(h);
+        out[2 * i] = f.x;
+        out[2 * i + 1] = f.y;
+      }
+    }
+  }
+}
+
+template <int DT>
+PQB_DEV float load1(const void* base, int64_t elem_off) {
+  return to_f32(static_cast<const typename DType<DT>::T*>(base)[elem_off]);
+}
+
+PQB_DEV float half_bits_to_f32(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+
+// ---------------------------------------------------------------- warp ops
+
+PQB_DEV float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+PQB_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+PQB_DEV unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ------------------------------------------------------- mbarrier + bulk copy
+// cp.async.bulk (SASS UBLKCP) moves a contiguous byte range global->shared on
+// the TMA engine and signals an mbarrier with the byte count on completion.
+
+PQB_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+PQB_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+PQB_DEV void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+PQB_DEV void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+PQB_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+PQB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+
+PQB_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
+  while (!mbar_try_wait(bar, phase)) {
+  }
+}
+
+PQB_DEV void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Streaming-data hint: bulk copy with an L2 evict-first policy.
+PQB_DEV void bulk_g2s_evict_first(void* smem_dst, const void* gmem_src, uint32_t bytes,
+                                  uint64_t* bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], "
+      "%2, [%3], %4;" ::"r"(smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+
+PQB_DEV uint64_t make_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+}  // namespace pqb

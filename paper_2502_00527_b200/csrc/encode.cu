@@ -1,0 +1,628 @@
+// HP-1: key-cache encoder kernels (sm_100a).
+//
+//   K1 radius_max_*      per-(unit, sub-channel) max of fl64(x^2 + y^2)
+//                        -> compute_radius_scales (polar_codec.py:236-251)
+//   K1' scales_finalize  fp16( fl32(sqrt(max)) / (2^n - 1) )   (polar_codec.py:250-251, 77-81)
+//   K2 encode_v8 / encode_generic
+//                        quantize_subvectors + pack_stream + _encode_block
+//                        (polar_codec.py:281-302, 98-110; kv_cache.py:191-197)
+//   store_values / store_residual / append
+//                        kv_cache.py:175-176, 179-189, 199-209
+//
+// Memory layout: keys are read with 128-bit loads, one thread per 8 consecutive
+// sub-channels of a token (x-half and y-half for HALF_SPLIT, one 8-pair run for
+// ADJACENT).  A warp therefore owns 256 consecutive codes = a contiguous 32*b-byte
+// span of each stream; the lanes assemble whole 32-bit words with warp shuffles
+// and write them with coalesced 32-bit stores straight into the paged store.
+#include "polar_math.cuh"
+#include "kernels.h"
+
+#include <algorithm>
+
+namespace pqb {
+
+PQB_DEV uint8_t* page_base(const pqb_store& s, int64_t unit, int64_t page) {
+  const int64_t pid = s.page_table ? static_cast<int64_t>(__ldg(s.page_table + unit * s.max_pages + page))
+                                   : unit * s.max_pages + page;
+  return s.pool + pid * s.page_bytes;
+}
+
+// Monotone map of a non-negative double to uint64 for atomicMax.
+PQB_DEV unsigned long long dbits(double v) { return static_cast<unsigned long long>(__double_as_longlong(v)); }
+
+PQB_DEV bool finite2(float x, float y) { return fabsf(x) <= 3.40282347e38f && fabsf(y) <= 3.40282347e38f; }
+
+// ------------------------------------------------------------------ K1
+
+template <int DT, int LAYOUT>
+__global__ void __launch_bounds__(256) radius_max_v8_kernel(const void* __restrict__ keys, int64_t T,
+                                                            int half, int64_t unit_stride,
+                                                            int64_t tok_stride, int64_t chunk,
+                                                            unsigned long long* __restrict__ maxsq,
+                                                            int32_t* __restrict__ flags) {
+  __shared__ double s_red[8][256];  // [channel-in-group][thread]
+  const int unit = blockIdx.y;
+  const int tpr = half >> 3;  // threads per token row
+  const int rows = 256 / tpr;
+  const int cg = threadIdx.x % tpr, row = threadIdx.x / tpr;
+  const int64_t t_begin = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t t_end = min(T, t_begin + chunk);
+  const int64_t ubase = static_cast<int64_t>(unit) * unit_stride;
+  double mx[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mx[i] = 0.0;
+  bool bad = false;
+  for (int64_t t = t_begin + row; t < t_end; t += rows) {
+    float x[8], y[8];
+    const int64_t rb = ubase + t * tok_stride;
+    if constexpr (LAYOUT == PQB_HALF_SPLIT) {
+      load8<DT>(keys, rb + 8 * cg, x);
+      load8<DT>(keys, rb + half + 8 * cg, y);
+    } else {
+      float v0[8], v1[8];
+      load8<DT>(keys, rb + 16 * cg, v0);
+      load8<DT>(keys, rb + 16 * cg + 8, v1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        x[i] = v0[2 * i]; y[i] = v0[2 * i + 1];
+        x[4 + i] = v1[2 * i]; y[4 + i] = v1[2 * i + 1];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      bad |= !finite2(x[i], y[i]);
+      const double xd = x[i], yd = y[i];
+      mx[i] = fmax(mx[i], __fma_rn(xd, xd, __dmul_rn(yd, yd)));
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, PQB_FLAG_NONFINITE);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s_red[i][threadIdx.x] = mx[i];
+  __syncthreads();
+  // thread c < half reduces channel c over all rows
+  for (int c = threadIdx.x; c < half; c += 256) {
+    const int g = c >> 3, i = c & 7;
+    double m = 0.0;
+    for (int r = 0; r < rows; ++r) m = fmax(m, s_red[i][r * tpr + g]);
+    if (m > 0.0) atomicMax(maxsq + static_cast<int64_t>(unit) * half + c, dbits(m));
+  }
+}
+
+// Any even d / layout / stride / alignment; one element pair per thread step.
+template <int DT>
+__global__ void __launch_bounds__(256) radius_max_generic_kernel(const void* __restrict__ keys, int64_t T,
+                                                                 int half, int layout,
+                                                                 int64_t unit_stride, int64_t tok_stride,
+                                                                 int64_t chunk,
+                                                                 unsigned long long* __restrict__ maxsq,
+                                                                 int32_t* __restrict__ flags) {
+  extern __shared__ unsigned long long s_max[];  // [half]
+  const int unit = blockIdx.y;
+  for (int c = threadIdx.x; c < half; c += blockDim.x) s_max[c] = 0ull;
+  __syncthreads();
+  const int64_t f_begin = static_cast<int64_t>(blockIdx.x) * chunk * half;
+  const int64_t f_end = min(T * half, f_begin + chunk * half);
+  const int64_t ubase = static_cast<int64_t>(unit) * unit_stride;
+  bool bad = false;
+  for (int64_t f = f_begin + threadIdx.x; f < f_end; f += blockDim.x) {
+    const int64_t t = f / half;
+    const int j = static_cast<int>(f - t * half);
+    const int64_t rb = ubase + t * tok_stride;
+    const int64_t ex = layout == PQB_HALF_SPLIT ? j : 2 * j;
+    const int64_t ey = layout == PQB_HALF_SPLIT ? j + half : 2 * j + 1;
+    const float x = load1<DT>(keys, rb + ex), y = load1<DT>(keys, rb + ey);
+    bad |= !finite2(x, y);
+    const double xd = x, yd = y;
+    const double d2 = __fma_rn(xd, xd, __dmul_rn(yd, yd));
+    if (d2 > 0.0) atomicMax(s_max + j, dbits(d2));
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, PQB_FLAG_NONFINITE);
+  __syncthreads();
+  for (int c = threadIdx.x; c < half; c += blockDim.x)
+    if (s_max[c]) atomicMax(maxsq + static_cast<int64_t>(unit) * half + c, s_max[c]);
+}
+
+__global__ void scales_finalize_kernel(const unsigned long long* __restrict__ maxsq, int64_t count,
+                                       int n_bits, uint16_t* __restrict__ scales,
+                                       int32_t* __restrict__ flags) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double d2 = __longlong_as_double(static_cast<long long>(maxsq[i]));
+  const float top = __double2float_rn(__dsqrt_rn(d2));                 // radius.max(axis=0), fp32
+  const float s = __fdiv_rn(top, static_cast<float>((1 << n_bits) - 1));  // fp32 / int
+  const __half h = __float2half_rn(s);                                  // ChannelScales -> fp16
+  if (__hisinf(h) || __hisnan(h)) atomicOr(flags, PQB_FLAG_SCALE_OVERFLOW);
+  scales[i] = __half_as_ushort(h);
+}
+
+// ------------------------------------------------------------------ K2
+
+// Word `w` of the bit string formed by concatenating the lanes' `cb`-bit chunks
+// (cb = 8*b, lane order).  Warp-collective: every lane must call with the same
+// `cb`; lanes pass their own w (only lanes with w < 8*b use the result).
+PQB_DEV uint32_t warp_word(unsigned long long chunk, int cb, int nch, int w) {
+  const int bit = 32 * w;
+  const int c0 = bit / cb;
+  const int o = bit - c0 * cb;
+  unsigned long long v = 0ull;
+  int have = 0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < nch) {  // warp-uniform
+      const unsigned long long cv = __shfl_sync(0xffffffffu, chunk, (c0 + k) & 31);
+      if (k == 0) {
+        v = cv >> o;
+        have = cb - o;
+      } else if (have < 32 && c0 + k < 32) {
+        v |= cv << have;
+        have += cb;
+      }
+    }
+  }
+  return static_cast<uint32_t>(v);
+}
+
+PQB_DEV int chunks_per_word(int b) { return b == 1 ? 4 : (b == 2 ? 2 : ((b == 4 || b == 8) ? 1 : 2)); }
+
+template <int DT, int LAYOUT, int M>
+__global__ void __launch_bounds__(256) encode_v8_kernel(const void* __restrict__ keys, int64_t T, int half,
+                                                        int64_t unit_stride, int64_t tok_stride,
+                                                        int64_t chunk, int n_bits,
+                                                        const uint16_t* __restrict__ scales, pqb_store st,
+                                                        const int32_t* __restrict__ tok_offset,
+                                                        int64_t tok_offset_const,
+                                                        unsigned long long* __restrict__ clamp_counts,
+                                                        int32_t* __restrict__ flags) {
+  __shared__ float s_tan[32], s_thr[32];
+  __shared__ unsigned int s_clamp;
+  if (threadIdx.x < 32) {
+    s_tan[threadIdx.x] = kEdgeTan[M][threadIdx.x];
+    s_thr[threadIdx.x] = kEdgeThr[M][threadIdx.x];
+  }
+  if (threadIdx.x == 0) s_clamp = 0u;
+  __syncthreads();
+  const int unit = blockIdx.y;
+  const int lane = threadIdx.x & 31;
+  const int tpr = half >> 3;
+  const int rows = 256 / tpr;
+  const int cg = threadIdx.x % tpr, row = threadIdx.x / tpr;
+  const int warp_row0 = (threadIdx.x >> 5) * (32 / tpr);
+  const int64_t off = (tok_offset ? static_cast<int64_t>(tok_offset[unit]) : 0) + tok_offset_const;
+  const int64_t t_begin = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t t_end = min(T, t_begin + chunk);
+  const int64_t ubase = static_cast<int64_t>(unit) * unit_stride;
+
+  float s32[8], inv[8];
+  {
+    const uint4 sv = __ldg(reinterpret_cast<const uint4*>(scales + static_cast<int64_t>(unit) * half + 8 * cg));
+    const uint32_t w[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      s32[2 * i] = half_bits_to_f32(static_cast<uint16_t>(w[i] & 0xffffu));
+      s32[2 * i + 1] = half_bits_to_f32(static_cast<uint16_t>(w[i] >> 16));
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) inv[i] = s32[i] > 0.0f ? __frcp_rn(s32[i]) : 0.0f;
+  }
+  const int wpt_a = half * M / 32, wpt_r = half * n_bits / 32;  // 32-bit words per token
+  const int cb_a = 8 * M, cb_r = 8 * n_bits;
+  const int nch_a = chunks_per_word(M), nch_r = chunks_per_word(n_bits);
+  const int64_t page_tok = st.page_tokens;
+  uint32_t clamps = 0;
+  bool bad = false;
+
+  for (int64_t base = t_begin; base < t_end; base += rows) {
+    const int64_t t = base + row;
+    const bool valid = t < t_end;
+    float x[8], y[8];
+    if (valid) {
+      const int64_t rb = ubase + t * tok_stride;
+      if constexpr (LAYOUT == PQB_HALF_SPLIT) {
+        load8<DT>(keys, rb + 8 * cg, x);
+        load8<DT>(keys, rb + half + 8 * cg, y);
+      } else {
+        float v0[8], v1[8];
+        load8<DT>(keys, rb + 16 * cg, v0);
+        load8<DT>(keys, rb + 16 * cg + 8, v1);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          x[i] = v0[2 * i]; y[i] = v0[2 * i + 1];
+          x[4 + i] = v1[2 * i]; y[4 + i] = v1[2 * i + 1];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) x[i] = y[i] = 0.0f;
+    }
+    unsigned long long ca = 0ull, cr = 0ull;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      bad |= !finite2(x[i], y[i]);
+      uint32_t a, r;
+      encode_pair<M>(x[i], y[i], s32[i], inv[i], n_bits, a, r, clamps, s_tan, s_thr);
+      ca |= static_cast<unsigned long long>(a) << (M * i);
+      cr |= static_cast<unsigned long long>(r) << (n_bits * i);
+    }
+    if (!valid) ca = cr = 0ull;
+    // ---- assemble and store the warp's 8*M angle words and 8*n radius words
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      const int b = pass == 0 ? M : n_bits;
+      const int cb = pass == 0 ? cb_a : cb_r;
+      const int nch = pass == 0 ? nch_a : nch_r;
+      const int wpt = pass == 0 ? wpt_a : wpt_r;
+      const int64_t region = pass == 0 ? st.angle_off : st.radius_off;
+      const unsigned long long chunk_bits = pass == 0 ? ca : cr;
+      for (int w0 = 0; w0 < 8 * b; w0 += 32) {  // warp-uniform
+        const int w = w0 + lane;
+        const uint32_t word = warp_word(chunk_bits, cb, nch, w);
+        if (w < 8 * b) {
+          const int tw = w / wpt;
+          const int64_t t_call = base + warp_row0 + tw;
+          if (t_call < t_end) {
+            const int64_t t_abs = off + t_call;
+            const int64_t page = t_abs / page_tok;
+            uint8_t* p = page_base(st, unit, page) + region +
+                         ((t_abs - page * page_tok) * wpt + (w - tw * wpt)) * 4;
+            *reinterpret_cast<uint32_t*>(p) = word;
+          }
+        }
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, PQB_FLAG_NONFINITE);
+  if (clamp_counts) {
+    unsigned int c = clamps;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0 && c) atomicAdd(&s_clamp, c);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_clamp) atomicAdd(clamp_counts + unit, static_cast<unsigned long long>(s_clamp));
+  }
+}
+
+// Generic encoder: any even d, any layout/stride, runtime bits, exact path.
+// Each warp owns 32 consecutive (absolute) flat codes; their b*32 bits are
+// b whole words of the stream.  Words not fully covered by this call's tokens
+// are merged with atomicOr (fresh pages are zero).
+struct GenericSrc {
+  const void* keys;  // [unit][t][d] with strides (elements)
+  int dtype;
+  int64_t unit_stride, tok_stride;
+};
+
+template <int DT>
+PQB_DEV float ld_any(const void* p, int64_t off) { return load1<DT>(p, off); }
+
+PQB_DEV float load_elem(const GenericSrc& s, int64_t off) {
+  switch (s.dtype) {
+    case PQB_F32: return ld_any<PQB_F32>(s.keys, off);
+    case PQB_BF16: return ld_any<PQB_BF16>(s.keys, off);
+    default: return ld_any<PQB_F16>(s.keys, off);
+  }
+}
+
+// Encode flat codes [32*g, 32*g + 32) of `unit` whose token range of this call
+// is [tok0, tok0 + T) (absolute).  Keys of call-token t at src row t.
+PQB_DEV void encode_group_exact(const GenericSrc& src, int64_t unit, int64_t g, int64_t tok0, int64_t T,
+                                int half, int layout, int m_bits, int n_bits, const float* s32_row,
+                                const pqb_store& st, uint32_t& clamps, bool& bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t f = 32 * g + lane;
+  const int64_t t_abs = f / half;
+  const int j = static_cast<int>(f - t_abs * half);
+  const int64_t t_call = t_abs - tok0;
+  const bool valid = t_call >= 0 && t_call < T;
+  uint32_t a = 0u, r = 0u;
+  if (valid) {
+    const int64_t rb = unit * src.unit_stride + t_call * src.tok_stride;
+    const int64_t ex = layout == PQB_HALF_SPLIT ? j : 2 * j;
+    const int64_t ey = layout == PQB_HALF_SPLIT ? j + half : 2 * j + 1;
+    const float x = load_elem(src, rb + ex), y = load_elem(src, rb + ey);
+    bad |= !finite2(x, y);
+    encode_pair_exact(x, y, s32_row[j], m_bits, n_bits, a, r, clamps);
+  }
+  const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+  if (vmask == 0u) return;
+  const int64_t page_tok = st.page_tokens;
+  const int64_t page = (32 * g) / (page_tok * half);
+  const int64_t g_in_page = g - page * page_tok * half / 32;
+  uint8_t* pbase = page_base(st, unit, page);
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+    const int b = pass == 0 ? m_bits : n_bits;
+    const uint32_t code = pass == 0 ? a : r;
+    uint32_t* words = reinterpret_cast<uint32_t*>(pbase + (pass == 0 ? st.angle_off : st.radius_off)) +
+                      g_in_page * b;
+    for (int w = 0; w < b; ++w) {
+      const int kb = 32 * w + lane;  // my bit in word w
+      const uint32_t c = __shfl_sync(0xffffffffu, code, kb / b);
+      const uint32_t word = __ballot_sync(0xffffffffu, (c >> (kb % b)) & 1u);
+      // lanes (codes) touching word w: [32w/b, (32w+31)/b]
+      const int lo = (32 * w) / b, hi = (32 * w + 31) / b;
+      const unsigned need = (hi >= 31 ? 0xffffffffu : ((2u << hi) - 1u)) & ~((1u << lo) - 1u);
+      if (lane == 0) {
+        if ((vmask & need) == need) words[w] = word;
+        else if (vmask & need) atomicOr(words + w, word);
+      }
+    }
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(256) encode_generic_kernel(GenericSrc src, int64_t T, int half, int layout,
+                                                             int m_bits, int n_bits,
+                                                             const uint16_t* __restrict__ scales, pqb_store st,
+                                                             const int32_t* __restrict__ tok_offset,
+                                                             int64_t tok_offset_const, int64_t groups_per_block,
+                                                             unsigned long long* __restrict__ clamp_counts,
+                                                             int32_t* __restrict__ flags) {
+  extern __shared__ float s_scale[];  // [half]
+  const int64_t unit = blockIdx.y;
+  for (int c = threadIdx.x; c < half; c += blockDim.x)
+    s_scale[c] = half_bits_to_f32(scales[unit * half + c]);
+  __syncthreads();
+  const int64_t tok0 = (tok_offset ? static_cast<int64_t>(tok_offset[unit]) : 0) + tok_offset_const;
+  const int64_t f_lo = tok0 * half, f_hi = (tok0 + T) * half;
+  const int64_t g_lo = f_lo / 32, g_hi = (f_hi + 31) / 32;
+  const int64_t gb = g_lo + static_cast<int64_t>(blockIdx.x) * groups_per_block;
+  const int64_t ge = min(g_hi, gb + groups_per_block);
+  uint32_t clamps = 0;
+  bool bad = false;
+  const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  for (int64_t g = gb + warp; g < ge; g += nwarps)
+    encode_group_exact(src, unit, g, tok0, T, half, layout, m_bits, n_bits, s_scale, st, clamps, bad);
+  const int lane = threadIdx.x & 31;
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, PQB_FLAG_NONFINITE);
+  if (clamp_counts) {
+    unsigned int c = clamps;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0 && c) atomicAdd(clamp_counts + unit, static_cast<unsigned long long>(c));
+  }
+}
+
+// ------------------------------------------------------------- values
+
+__global__ void store_values_kernel(const void* __restrict__ vals, int src_dtype, int64_t T, int d,
+                                    int64_t unit_stride, int64_t tok_stride, pqb_store st,
+                                    const int32_t* __restrict__ tok_offset, int64_t tok_offset_const) {
+  const int64_t unit = blockIdx.y;
+  const int64_t off = (tok_offset ? static_cast<int64_t>(tok_offset[unit]) : 0) + tok_offset_const;
+  const int64_t n = T * d;
+  const int vbytes = st.value_dtype == PQB_F32 ? 4 : 2;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / d;
+    const int e = static_cast<int>(i - t * d);
+    float v = 0.0f;
+    if (vals) {
+      const int64_t so = unit * unit_stride + t * tok_stride + e;
+      v = src_dtype == PQB_F32 ? load1<PQB_F32>(vals, so)
+                               : (src_dtype == PQB_BF16 ? load1<PQB_BF16>(vals, so) : load1<PQB_F16>(vals, so));
+    }
+    const int64_t ta = off + t;
+    const int64_t page = ta / st.page_tokens;
+    uint8_t* p = page_base(st, unit, page) + st.value_off +
+                 ((ta - page * st.page_tokens) * d + e) * vbytes;
+    if (vbytes == 4) *reinterpret_cast<float*>(p) = v;
+    else *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
+  }
+}
+
+__global__ void store_residual_kernel(const void* __restrict__ keys, int src_dtype, int64_t T, int d,
+                                      int64_t unit_stride, int64_t tok_stride, float* __restrict__ ring,
+                                      int res_cap, int64_t tok_offset_const, int32_t* __restrict__ flags) {
+  const int64_t unit = blockIdx.y;
+  const int64_t n = T * d;
+  bool bad = false;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / d;
+    const int e = static_cast<int>(i - t * d);
+    const int64_t so = unit * unit_stride + t * tok_stride + e;
+    const float v = src_dtype == PQB_F32 ? load1<PQB_F32>(keys, so)
+                                         : (src_dtype == PQB_BF16 ? load1<PQB_BF16>(keys, so) : load1<PQB_F16>(keys, so));
+    bad |= !(fabsf(v) <= 3.40282347e38f);
+    const int64_t slot = (tok_offset_const + t) % res_cap;
+    ring[(unit * res_cap + slot) * d + e] = v;
+  }
+  if (bad) atomicOr(flags, PQB_FLAG_NONFINITE);
+}
+
+// ----------------------------------------------------------------- K5
+
+// One block per unit.  kv_cache.py:179-189 with the residual deque as a ring.
+__global__ void __launch_bounds__(256) append_kernel(pqb_cache c, const void* __restrict__ keys, int key_dtype,
+                                                     const void* __restrict__ vals, int val_dtype,
+                                                     unsigned long long* __restrict__ clamp_counts,
+                                                     int32_t* __restrict__ flags) {
+  extern __shared__ float s_scale[];  // [half]
+  const int64_t unit = blockIdx.x;
+  const int d = c.d, half = d / 2;
+  for (int j = threadIdx.x; j < half; j += blockDim.x) s_scale[j] = half_bits_to_f32(c.scales[unit * half + j]);
+  const int64_t T = c.seq_lens[unit], Tq = c.quant_lens[unit];
+  __syncthreads();
+  const bool flush = (T - Tq) >= c.res_cap;  // after the push the FIFO exceeds residual_len
+  uint32_t clamps = 0;
+  bool bad = false;
+  if (flush) {
+    GenericSrc src;
+    if (c.res_cap == 0) {
+      src.keys = keys; src.dtype = key_dtype; src.unit_stride = d; src.tok_stride = d;
+    } else {  // oldest residual key: token Tq lives in slot Tq % res_cap
+      src.keys = c.residual + (unit * c.res_cap + Tq % c.res_cap) * d;
+      src.dtype = PQB_F32; src.unit_stride = 0; src.tok_stride = d;
+    }
+    const int64_t g_lo = (Tq * half) / 32, g_hi = ((Tq + 1) * half + 31) / 32;
+    const int warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int64_t g = g_lo + warp; g < g_hi; g += nwarps)
+      encode_group_exact(src, unit, g, Tq, 1, half, c.layout, c.angle_bits, c.radius_bits, s_scale, c.store,
+                         clamps, bad);
+  }
+  __syncthreads();  // the flushed slot is read before it is overwritten
+  for (int e = threadIdx.x; e < d; e += blockDim.x) {
+    const int64_t ko = unit * d + e;
+    const float kv = key_dtype == PQB_F32 ? load1<PQB_F32>(keys, ko)
+                                          : (key_dtype == PQB_BF16 ? load1<PQB_BF16>(keys, ko) : load1<PQB_F16>(keys, ko));
+    bad |= !(fabsf(kv) <= 3.40282347e38f);
+    if (c.res_cap > 0) c.residual[(unit * c.res_cap + T % c.res_cap) * d + e] = kv;
+    if (c.store.value_off >= 0) {
+      float v = 0.0f;
+      if (vals)
+        v = val_dtype == PQB_F32 ? load1<PQB_F32>(vals, ko)
+                                 : (val_dtype == PQB_BF16 ? load1<PQB_BF16>(vals, ko) : load1<PQB_F16>(vals, ko));
+      const int64_t page = T / c.store.page_tokens;
+      uint8_t* p = page_base(c.store, unit, page) + c.store.value_off;
+      const int64_t idx = (T - page * c.store.page_tokens) * d + e;
+      if (c.store.value_dtype == PQB_F32) reinterpret_cast<float*>(p)[idx] = v;
+      else reinterpret_cast<__nv_bfloat16*>(p)[idx] = __float2bfloat16_rn(v);
+    }
+  }
+  if (bad) atomicOr(flags, PQB_FLAG_NONFINITE);
+  const int lane = threadIdx.x & 31;
+  unsigned int cl = clamps;
+  for (int o = 16; o > 0; o >>= 1) cl += __shfl_xor_sync(0xffffffffu, cl, o);
+  if (lane == 0 && cl && clamp_counts) atomicAdd(clamp_counts + unit, static_cast<unsigned long long>(cl));
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    c.seq_lens[unit] = static_cast<int32_t>(T + 1);
+    if (flush) c.quant_lens[unit] = static_cast<int32_t>(Tq + 1);
+  }
+}
+
+// ------------------------------------------------------------ launchers
+
+template <int DT, int LAYOUT>
+static void launch_rmax_v8(const RadiusScalesArgs& a, int64_t chunk, dim3 grid, cudaStream_t s) {
+  radius_max_v8_kernel<DT, LAYOUT><<<grid, 256, 0, s>>>(a.keys, a.tokens, a.d / 2, a.unit_stride, a.tok_stride,
+                                                        chunk, a.maxsq_ws, a.flags);
+}
+
+int launch_radius_scales(const RadiusScalesArgs& a, cudaStream_t s) {
+  const int half = a.d / 2;
+  cudaMemsetAsync(a.maxsq_ws, 0, sizeof(unsigned long long) * a.n_units * half, s);
+  const int64_t chunk = 4096;
+  dim3 grid(static_cast<unsigned>((a.tokens + chunk - 1) / chunk), static_cast<unsigned>(a.n_units));
+  if (a.vector_ok) {
+    switch (a.key_dtype * 2 + a.layout) {
+      case PQB_F32 * 2 + PQB_ADJACENT: launch_rmax_v8<PQB_F32, PQB_ADJACENT>(a, chunk, grid, s); break;
+      case PQB_F32 * 2 + PQB_HALF_SPLIT: launch_rmax_v8<PQB_F32, PQB_HALF_SPLIT>(a, chunk, grid, s); break;
+      case PQB_BF16 * 2 + PQB_ADJACENT: launch_rmax_v8<PQB_BF16, PQB_ADJACENT>(a, chunk, grid, s); break;
+      case PQB_BF16 * 2 + PQB_HALF_SPLIT: launch_rmax_v8<PQB_BF16, PQB_HALF_SPLIT>(a, chunk, grid, s); break;
+      case PQB_F16 * 2 + PQB_ADJACENT: launch_rmax_v8<PQB_F16, PQB_ADJACENT>(a, chunk, grid, s); break;
+      default: launch_rmax_v8<PQB_F16, PQB_HALF_SPLIT>(a, chunk, grid, s); break;
+    }
+  } else {
+    const size_t shm = sizeof(unsigned long long) * half;
+    switch (a.key_dtype) {
+      case PQB_F32:
+        radius_max_generic_kernel<PQB_F32><<<grid, 256, shm, s>>>(a.keys, a.tokens, half, a.layout, a.unit_stride,
+                                                                   a.tok_stride, chunk, a.maxsq_ws, a.flags);
+        break;
+      case PQB_BF16:
+        radius_max_generic_kernel<PQB_BF16><<<grid, 256, shm, s>>>(a.keys, a.tokens, half, a.layout, a.unit_stride,
+                                                                    a.tok_stride, chunk, a.maxsq_ws, a.flags);
+        break;
+      default:
+        radius_max_generic_kernel<PQB_F16><<<grid, 256, shm, s>>>(a.keys, a.tokens, half, a.layout, a.unit_stride,
+                                                                   a.tok_stride, chunk, a.maxsq_ws, a.flags);
+        break;
+    }
+  }
+  const int64_t count = a.n_units * half;
+  scales_finalize_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(a.maxsq_ws, count, a.radius_bits,
+                                                                                   a.scales_out, a.flags);
+  return 0;
+}
+
+template <int DT, int LAYOUT, int M>
+static void launch_enc_v8(const EncodeArgs& a, int64_t chunk, dim3 grid, cudaStream_t s) {
+  encode_v8_kernel<DT, LAYOUT, M><<<grid, 256, 0, s>>>(a.keys, a.tokens, a.d / 2, a.unit_stride, a.tok_stride,
+                                                       chunk, a.radius_bits, a.scales, *a.store, a.tok_offset,
+                                                       a.tok_offset_const, a.clamp_counts, a.flags);
+}
+
+template <int DT, int LAYOUT>
+static void dispatch_m(const EncodeArgs& a, int64_t chunk, dim3 grid, cudaStream_t s) {
+  switch (a.angle_bits) {
+    case 1: launch_enc_v8<DT, LAYOUT, 1>(a, chunk, grid, s); break;
+    case 2: launch_enc_v8<DT, LAYOUT, 2>(a, chunk, grid, s); break;
+    case 3: launch_enc_v8<DT, LAYOUT, 3>(a, chunk, grid, s); break;
+    case 4: launch_enc_v8<DT, LAYOUT, 4>(a, chunk, grid, s); break;
+    case 5: launch_enc_v8<DT, LAYOUT, 5>(a, chunk, grid, s); break;
+    case 6: launch_enc_v8<DT, LAYOUT, 6>(a, chunk, grid, s); break;
+    case 7: launch_enc_v8<DT, LAYOUT, 7>(a, chunk, grid, s); break;
+    default: launch_enc_v8<DT, LAYOUT, 8>(a, chunk, grid, s); break;
+  }
+}
+
+int launch_encode(const EncodeArgs& a, cudaStream_t s) {
+  const int half = a.d / 2;
+  if (a.tokens == 0) return 0;
+  if (a.vector_ok) {
+    const int64_t chunk = 2048;
+    dim3 grid(static_cast<unsigned>((a.tokens + chunk - 1) / chunk), static_cast<unsigned>(a.n_units));
+    switch (a.key_dtype * 2 + a.layout) {
+      case PQB_F32 * 2 + PQB_ADJACENT: dispatch_m<PQB_F32, PQB_ADJACENT>(a, chunk, grid, s); break;
+      case PQB_F32 * 2 + PQB_HALF_SPLIT: dispatch_m<PQB_F32, PQB_HALF_SPLIT>(a, chunk, grid, s); break;
+      case PQB_BF16 * 2 + PQB_ADJACENT: dispatch_m<PQB_BF16, PQB_ADJACENT>(a, chunk, grid, s); break;
+      case PQB_BF16 * 2 + PQB_HALF_SPLIT: dispatch_m<PQB_BF16, PQB_HALF_SPLIT>(a, chunk, grid, s); break;
+      case PQB_F16 * 2 + PQB_ADJACENT: dispatch_m<PQB_F16, PQB_ADJACENT>(a, chunk, grid, s); break;
+      default: dispatch_m<PQB_F16, PQB_HALF_SPLIT>(a, chunk, grid, s); break;
+    }
+  } else {
+    GenericSrc src{a.keys, a.key_dtype, a.unit_stride, a.tok_stride};
+    // groups spanned by one unit's call (upper bound, offsets are per unit)
+    const int64_t groups = (a.tokens * half) / 32 + 2;
+    const int64_t gpb = 64;
+    dim3 grid(static_cast<unsigned>((groups + gpb - 1) / gpb), static_cast<unsigned>(a.n_units));
+    const size_t shm = sizeof(float) * half;
+    switch (a.key_dtype) {
+      case PQB_F32:
+        encode_generic_kernel<PQB_F32><<<grid, 256, shm, s>>>(src, a.tokens, half, a.layout, a.angle_bits,
+                                                               a.radius_bits, a.scales, *a.store, a.tok_offset,
+                                                               a.tok_offset_const, gpb, a.clamp_counts, a.flags);
+        break;
+      case PQB_BF16:
+        encode_generic_kernel<PQB_BF16><<<grid, 256, shm, s>>>(src, a.tokens, half, a.layout, a.angle_bits,
+                                                                a.radius_bits, a.scales, *a.store, a.tok_offset,
+                                                                a.tok_offset_const, gpb, a.clamp_counts, a.flags);
+        break;
+      default:
+        encode_generic_kernel<PQB_F16><<<grid, 256, shm, s>>>(src, a.tokens, half, a.layout, a.angle_bits,
+                                                               a.radius_bits, a.scales, *a.store, a.tok_offset,
+                                                               a.tok_offset_const, gpb, a.clamp_counts, a.flags);
+        break;
+    }
+  }
+  return 0;
+}
+
+int launch_store_values(const void* vals, int dtype, int64_t n_units, int64_t T, int d, int64_t us, int64_t ts,
+                        const pqb_store& st, const int32_t* tok_offset, int64_t tok_offset_const, cudaStream_t s) {
+  if (T == 0) return 0;
+  const int64_t n = T * d;
+  dim3 grid(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096)), static_cast<unsigned>(n_units));
+  store_values_kernel<<<grid, 256, 0, s>>>(vals, dtype, T, d, us, ts, st, tok_offset, tok_offset_const);
+  return 0;
+}
+
+int launch_store_residual(const pqb_cache& c, const void* keys, int dtype, int64_t n_units, int64_t T, int64_t us,
+                          int64_t ts, int64_t tok_offset_const, int32_t* flags, cudaStream_t s) {
+  if (T == 0) return 0;
+  const int64_t n = T * c.d;
+  dim3 grid(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096)), static_cast<unsigned>(n_units));
+  store_residual_kernel<<<grid, 256, 0, s>>>(keys, dtype, T, c.d, us, ts, c.residual, c.res_cap, tok_offset_const,
+                                              flags);
+  return 0;
+}
+
+int launch_append(const pqb_cache& c, int64_t n_units, const void* keys, int key_dtype, const void* vals,
+                  int val_dtype, unsigned long long* clamp_counts, int32_t* flags, cudaStream_t s) {
+  const size_t shm = sizeof(float) * (c.d / 2);
+  append_kernel<<<static_cast<unsigned>(n_units), 128, shm, s>>>(c, keys, key_dtype, vals, val_dtype, clamp_counts,
+                                                                  flags);
+  return 0;
+}
+
+}  // namespace pqb

@@ -1,0 +1,196 @@
+// Exact float32 polar quantization (HP-1 arithmetic), sm_100a.
+//
+// Reference semantics (polar_codec.py, all float32 numpy):
+//   to_polar        :200-209  r = hypotf(x, y);  t = mod(atan2f(y, x) + pi, 2pi)
+//   quantize_angle  :212-221  code = rint(t * fl32(2^(m-1)/pi)) mod 2^m   (half-even)
+//   _quantize_radius_counted :267-278  raw = rint(r / s32); s32 == 0 -> 0; clamp to 2^n-1
+//   quantize_subvectors :281-302  rcode == 0 -> angle = 2^(m-1); s16 == 0 -> both 0
+//
+// "Exact" here means the reference pipeline evaluated with a correctly rounded
+// atan2f and glibc's hypotf (fl32(sqrt(fl64(x*x + y*y)))).  numpy's own float32
+// arctan2 is a SIMD approximation (<= a few ulp), so a reference code may differ
+// from ours only when the angle sits within ~1e-6 rad of a bin edge: the counted,
+// admissible "ties" of the parity contract.
+//
+// Fast path.  Evaluating atan2 in double for every element would make the
+// encoder FP64-bound, so the bin is decided geometrically: fold (x, y) into the
+// first octant (m >= 3; quadrant for m = 2), then count the bin edges b_i below
+// the point with one FMA each, D_i = mn - mx * tan(b_i).  A point farther than
+// DELTA = 4e-6 rad from every edge gets the same code as the exact pipeline:
+// the pipeline's total drift from the true angle is <= 1.0e-6 rad
+//   (|pi_f32 - pi| = 8.7e-8, atan2 rounding 1.2e-7, t rounding 2.4e-7,
+//    fl32(2^(m-1)/pi) relative 6e-8 -> 3.7e-7, product rounding 1.9e-7)
+// and D_i's own float error is < 2e-7 r.  Points inside the band (about 1e-5
+// of random inputs) take the exact double-precision path.  The radius uses the
+// same scheme: a fast fp32 estimate of r/s, and the exact path only when the
+// estimate lies within 2^-18 relative of a rounding boundary.
+#pragma once
+
+#include "common.cuh"
+#include "angle_tables.h"
+
+namespace pqb {
+
+constexpr float kPiF = 3.14159274101257324219f;     // fl32(pi)
+constexpr float kTwoPiF = 6.28318548202514648438f;  // fl32(2 pi) == 2 * fl32(pi)
+
+// ------------------------------------------------------------ exact paths
+
+PQB_DEV uint32_t angle_code_exact(float x, float y, int m) {
+  const float a = __double2float_rn(atan2(static_cast<double>(y), static_cast<double>(x)));
+  float t = __fadd_rn(a, kPiF);
+  if (t >= kTwoPiF) t = 0.0f;  // np.mod(t, fl32(2 pi)); t <= 2 pi_f32 by construction
+  const float u = __fmul_rn(t, kAngleScale[m]);
+  return static_cast<uint32_t>(__float2int_rn(u)) & ((1u << m) - 1u);
+}
+
+// fl32(sqrt(fl64(x^2 + y^2))): both squares are exact in double, one rounding
+// in the sum, glibc's hypotf (sysdeps/ieee754/flt-32/e_hypotf.c) order.
+PQB_DEV float radius_exact(float x, float y) {
+  const double xd = x, yd = y;
+  const double d2 = __fma_rn(xd, xd, __dmul_rn(yd, yd));
+  return __double2float_rn(__dsqrt_rn(d2));
+}
+
+// rint(fl32(r / s)) as a float (may be +inf); s > 0.
+PQB_DEV float radius_raw_exact(float x, float y, float s) {
+  return rintf(__fdiv_rn(radius_exact(x, y), s));
+}
+
+// ------------------------------------------------------------- fast paths
+
+// Angle code for angle_bits M; sets amb when the point is within DELTA of a bin
+// edge (or the input magnitude is outside the range where the fp32 edge test is
+// reliable) and the caller must use angle_code_exact.
+template <int M>
+PQB_DEV uint32_t angle_code_fast(float x, float y, bool& amb, const float* smem_tan,
+                                 const float* smem_thr) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const uint32_t sx = __float_as_uint(x) >> 31, sy = __float_as_uint(y) >> 31;
+  if constexpr (M == 1) {
+    // edges at phi = +-pi/2 (the y axis): code 1 iff x > 0
+    const float mx = fmaxf(ax, ay);
+    amb = !(ax > PQB_ANGLE_DELTA * (ax + ay)) || !(mx >= 0x1p-100f && mx <= 0x1p100f);
+    return sx ? 0u : 1u;
+  } else {
+    constexpr int H = 1 << (M - 1);
+    int k;  // bin index within the quadrant, 0 .. 2^(M-2)
+    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+    amb = !(mx >= 0x1p-100f && mx <= 0x1p100f);
+    if constexpr (M == 2) {
+      const float dd = ay - ax;  // edge at pi/4; sign exact
+      amb |= fabsf(dd) <= kQuadEdgeThr * (ax + ay);
+      k = dd > 0.0f ? 1 : 0;
+    } else {
+      constexpr int NB = 1 << (M - 3);  // octant edges
+      const float sum = mx + mn;
+      int kk = 0;
+      if constexpr (NB <= 4) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          const float di = fmaf(-mx, kEdgeTan[M][i], mn);
+          kk += di > 0.0f ? 1 : 0;
+          amb |= fabsf(di) <= kEdgeThr[M][i] * sum;
+        }
+      } else {
+        // estimate psi = atan(mn/mx) to < step/4, then verify the two edges
+        // around the estimated bin exactly.
+        constexpr float kInvStep = static_cast<float>(1 << (M - 1)) / 3.14159265358979f;
+        const float rho = mn * __frcp_rn(mx);
+        // atan(rho) ~ rho*(pi/4 + 0.273*(1 - rho)), |err| < 4e-3 rad on [0, 1]
+        const float psi = rho * fmaf(0.2732395f, 1.0f - rho, 0.78539816f);
+        int ke = __float2int_rn(psi * kInvStep);
+        ke = ke < 0 ? 0 : (ke > NB ? NB : ke);
+        kk = ke;
+        if (ke > 0) {  // edge below: b_{ke-1}
+          const float di = fmaf(-mx, smem_tan[ke - 1], mn);
+          kk -= di > 0.0f ? 0 : 1;
+          amb |= fabsf(di) <= smem_thr[ke - 1] * sum;
+        }
+        if (ke < NB) {  // edge above: b_ke
+          const float di = fmaf(-mx, smem_tan[ke], mn);
+          kk += di > 0.0f ? 1 : 0;
+          amb |= fabsf(di) <= smem_thr[ke] * sum;
+        }
+      }
+      constexpr int Q = 1 << (M - 2);
+      k = (ay > ax) ? (Q - kk) : kk;  // unfold the octant
+    }
+    // unfold the quadrant: code = (c_phi + H) mod 2H with c_phi the multiple of
+    // the grid step nearest phi = atan2(y, x)
+    const int base = sx ? (sy ? 0 : 2 * H) : H;
+    const int c = (sx ^ sy) ? base - k : base + k;
+    return static_cast<uint32_t>(c) & (2u * H - 1u);
+  }
+}
+
+// Fast radius raw code rint(r/s) for s > 0 (as a float; large values mean
+// "clamped").  Sets amb when the estimate is too close to a rounding edge or the
+// magnitude is outside the safe fp32 range.
+PQB_DEV float radius_raw_fast(float x, float y, float inv_s, bool& amb) {
+  if (x == 0.0f && y == 0.0f) {
+    amb = false;
+    return 0.0f;
+  }
+  const float r2 = fmaf(x, x, y * y);
+  amb = !(r2 >= 0x1p-100f && r2 <= 0x1p100f);
+  const float q = r2 * rsqrtf(r2) * inv_s;
+  if (q >= 1024.0f) return q;  // far above any top code (<= 255): certainly clamped
+  const float fl = floorf(q);
+  const float fr = q - fl;
+  amb |= fabsf(fr - 0.5f) <= 0x1p-18f * q;
+  return fr > 0.5f ? fl + 1.0f : fl;
+}
+
+// Full per-sub-vector encode (quantize_subvectors semantics) with the fast path
+// and exact fallback.  s32 is the fp16 scale widened to f32; inv_s = 1/s32.
+template <int M>
+PQB_DEV void encode_pair(float x, float y, float s32, float inv_s, int n_bits, uint32_t& acode,
+                         uint32_t& rcode, uint32_t& clamped, const float* smem_tan,
+                         const float* smem_thr) {
+  if (s32 == 0.0f) {  // zero-scale channel: both codes 0 (polar_codec.py:298-301)
+    acode = 0u;
+    rcode = 0u;
+    return;
+  }
+  const float top = static_cast<float>((1 << n_bits) - 1);
+  bool ramb;
+  float raw = radius_raw_fast(x, y, inv_s, ramb);
+  if (ramb) raw = radius_raw_exact(x, y, s32);
+  if (raw > top) {
+    clamped += 1u;
+    raw = top;
+  }
+  rcode = static_cast<uint32_t>(raw);
+  if (rcode == 0u) {  // canonical: origin's angle code (polar_codec.py:297)
+    acode = 1u << (M - 1);
+    return;
+  }
+  bool aamb;
+  acode = angle_code_fast<M>(x, y, aamb, smem_tan, smem_thr);
+  if (aamb) acode = angle_code_exact(x, y, M);
+}
+
+// Runtime-m variant: exact pipeline only (used by the generic / append paths).
+PQB_DEV void encode_pair_exact(float x, float y, float s32, int m_bits, int n_bits,
+                               uint32_t& acode, uint32_t& rcode, uint32_t& clamped) {
+  if (s32 == 0.0f) {
+    acode = 0u;
+    rcode = 0u;
+    return;
+  }
+  const float top = static_cast<float>((1 << n_bits) - 1);
+  float raw = radius_raw_exact(x, y, s32);
+  if (raw > top) {
+    clamped += 1u;
+    raw = top;
+  }
+  rcode = static_cast<uint32_t>(raw);
+  if (rcode == 0u) {
+    acode = 1u << (m_bits - 1);
+    return;
+  }
+  acode = angle_code_exact(x, y, m_bits);
+}
+
+}  // namespace pqb
