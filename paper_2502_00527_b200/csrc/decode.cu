@@ -280,27 +280,27 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 #pragma unroll
   for (int g = 0; g < G; ++g) l_run[g] = warp_sum(l_run[g]);
   __syncthreads();
-  float* red = reinterpret_cast<float*>(warp_area);  // [NW][G][2 + 128]
-  float* mine = red + warp * G * 130;
+  float* red = reinterpret_cast<float*>(warp_area);  // [NW][G][4 + 128]: m, l, pad, o
+  float* mine = red + warp * G * 132;
 #pragma unroll
   for (int g = 0; g < G; ++g) {
-    if (lane == 0) { mine[g * 130] = m_run[g]; mine[g * 130 + 1] = l_run[g]; }
-    *reinterpret_cast<float4*>(mine + g * 130 + 2 + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+    if (lane == 0) { mine[g * 132] = m_run[g]; mine[g * 132 + 1] = l_run[g]; }
+    *reinterpret_cast<float4*>(mine + g * 132 + 4 + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
   }
   __syncthreads();
   for (int i = tid; i < G * 128; i += blockDim.x) {
     const int g = i >> 7, e = i & 127;
     float mx = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, red[(w * G + g) * 130]);
+    for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, red[(w * G + g) * 132]);
     float L = 0.0f, O = 0.0f;
     if (mx != -INFINITY) {
 #pragma unroll
       for (int w = 0; w < kNW; ++w) {
-        const float* rw = red + (w * G + g) * 130;
+        const float* rw = red + (w * G + g) * 132;
         const float sc = exp2f(rw[0] - mx);
         L = fmaf(rw[1], sc, L);
-        O = fmaf(rw[2 + e], sc, O);
+        O = fmaf(rw[4 + e], sc, O);
       }
     }
     if (ep.n_splits == 1) {

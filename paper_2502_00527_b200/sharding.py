@@ -1,0 +1,158 @@
+"""Multi-GPU placement of cache units and the per-layer head-output gather.
+
+Every (layer, sequence, kv-head) unit is independent in both hot paths
+(scales are per unit, kv_cache.py:171; query head hq reads only kv head
+hq // G), so the cache shards without any data-path exchange:
+
+* batch sharding  -- each rank owns whole sequences (all layers, all heads):
+                     no collective at all; the benchmark's default (weak scaling).
+* head sharding   -- each rank owns a contiguous block of KV heads (and, when
+                     there are more ranks than KV heads, a slice of the batch).
+                     A layer's attention output then spans ranks, so the
+                     per-layer [B, Hq, d] output is all-gathered (NCCL over
+                     NVLink on the GPU box; gloo in the CPU tests).  This is the
+                     only collective on the path (configs[2], configs[3]).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+
+@dataclass(frozen=True)
+class DecodeShape:
+    layers: int
+    batch: int
+    q_heads: int
+    kv_heads: int
+    head_dim: int = 128
+
+    def __post_init__(self) -> None:
+        if self.q_heads % self.kv_heads:
+            raise ValueError(f"q_heads {self.q_heads} not a multiple of kv_heads {self.kv_heads}")
+
+    @property
+    def group(self) -> int:
+        return self.q_heads // self.kv_heads
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    """Units owned by one rank: layers x sequences [b0, b1) x kv heads [h0, h1)."""
+
+    shape: DecodeShape
+    world: int
+    rank: int
+    b0: int
+    b1: int
+    h0: int
+    h1: int
+
+    @property
+    def batch(self) -> int:
+        return self.b1 - self.b0
+
+    @property
+    def kv_heads(self) -> int:
+        return self.h1 - self.h0
+
+    @property
+    def units_per_layer(self) -> int:
+        return self.batch * self.kv_heads
+
+    @property
+    def n_units(self) -> int:
+        return self.shape.layers * self.units_per_layer
+
+    def unit_index(self, layer: int, b: int, h: int) -> int:
+        """Local unit id of global (layer, sequence b, kv head h); layer-major,
+        then sequence, then head -- a layer is a contiguous unit range."""
+        if not (self.b0 <= b < self.b1 and self.h0 <= h < self.h1):
+            raise KeyError((layer, b, h))
+        return (layer * self.batch + (b - self.b0)) * self.kv_heads + (h - self.h0)
+
+    def owns(self, layer: int, b: int, h: int) -> bool:
+        return self.b0 <= b < self.b1 and self.h0 <= h < self.h1 and 0 <= layer < self.shape.layers
+
+
+def batch_shard(shape: DecodeShape, world: int, rank: int) -> ShardPlan:
+    """Contiguous sequence blocks; all heads local (no collective)."""
+    if shape.batch % world:
+        raise ValueError(f"batch {shape.batch} not divisible by world {world}")
+    per = shape.batch // world
+    return ShardPlan(shape, world, rank, rank * per, (rank + 1) * per, 0, shape.kv_heads)
+
+
+def head_shard(shape: DecodeShape, world: int, rank: int) -> ShardPlan:
+    """KV-head blocks; with more ranks than KV heads each head's sequences are
+    split further (world = kv_heads * batch_groups)."""
+    H = shape.kv_heads
+    if world <= H:
+        if H % world:
+            raise ValueError(f"kv_heads {H} not divisible by world {world}")
+        per = H // world
+        return ShardPlan(shape, world, rank, 0, shape.batch, rank * per, (rank + 1) * per)
+    if world % H or shape.batch % (world // H):
+        raise ValueError(f"world {world} must be kv_heads x a divisor of batch")
+    groups = world // H
+    h, g = rank // groups, rank % groups
+    per_b = shape.batch // groups
+    return ShardPlan(shape, world, rank, g * per_b, (g + 1) * per_b, h, h + 1)
+
+
+def local_queries(q_layer: torch.Tensor, plan: ShardPlan) -> torch.Tensor:
+    """[B, Hq, d] query rows of one layer -> this rank's [units_per_layer, G, d]."""
+    G = plan.shape.group
+    q = q_layer[plan.b0 : plan.b1, plan.h0 * G : plan.h1 * G]
+    return q.reshape(plan.batch * plan.kv_heads, G, q_layer.shape[-1]).contiguous()
+
+
+def gather_head_outputs(local_out: torch.Tensor, plan: ShardPlan, group=None) -> torch.Tensor:
+    """All-gather one layer's attention output.
+
+    local_out: [units_per_layer, G, d] in this rank's (sequence, head) order.
+    Returns the full [B, Hq, d] on every rank (GQA head order hq = h*G + g)."""
+    import torch.distributed as dist
+
+    S = plan.shape
+    G, d = S.group, local_out.shape[-1]
+    blk = local_out.reshape(plan.batch, plan.kv_heads, G, d).contiguous()
+    if dist.get_backend(group) == "nccl":
+        buf = torch.empty((plan.world,) + tuple(blk.shape), dtype=blk.dtype, device=blk.device)
+        dist.all_gather_into_tensor(buf, blk, group=group)
+        parts = list(buf.unbind(0))
+    else:
+        parts = [torch.empty_like(blk) for _ in range(plan.world)]
+        dist.all_gather(parts, blk, group=group)
+    full = torch.empty((S.batch, S.kv_heads, G, d), dtype=blk.dtype, device=blk.device)
+    for r, part in enumerate(parts):
+        p = plan_for(S, plan.world, r, head=True)
+        full[p.b0 : p.b1, p.h0 : p.h1] = part
+    return full.reshape(S.batch, S.q_heads, d)
+
+
+def plan_for(shape: DecodeShape, world: int, rank: int, head: bool) -> ShardPlan:
+    return head_shard(shape, world, rank) if head else batch_shard(shape, world, rank)
+
+
+class HeadShardedDecoder:
+    """Per-rank decode over a head-sharded cache + the per-layer NCCL gather.
+
+    ``cache`` is this rank's PolarKVCache holding plan.n_units units in
+    plan.unit_index order; ``step(q)`` runs all layers for q [L, B, Hq, d] and
+    returns the gathered [L, B, Hq, d] outputs."""
+
+    def __init__(self, cache, plan: ShardPlan, group=None, out_dtype=torch.bfloat16) -> None:
+        self.cache, self.plan, self.group = cache, plan, group
+        upl = plan.units_per_layer
+        self.views = [cache.view(layer * upl, (layer + 1) * upl) for layer in range(plan.shape.layers)]
+        self.out_dtype = out_dtype
+
+    def layer(self, layer: int, q_layer: torch.Tensor) -> torch.Tensor:
+        local = self.views[layer].decode(local_queries(q_layer, self.plan), out_dtype=self.out_dtype)
+        return gather_head_outputs(local, self.plan, self.group)
+
+    def step(self, q: torch.Tensor) -> torch.Tensor:
+        return torch.stack([self.layer(layer, q[layer]) for layer in range(self.plan.shape.layers)])

@@ -61,7 +61,10 @@ def test_golden_cache_scores_and_attention(golden, idx):
         w = pq.attention_weights(sc, temp)
         np.testing.assert_allclose(w.sum(), 1.0, atol=1e-12)
         if not tie.any():
-            np.testing.assert_allclose(w, c["weights"][g], rtol=1e-10, atol=1e-15)
+            # residual-token scores are fp32 dots whose summation order differs
+            # from BLAS (1e-5 peak-relative); quantized-only weights match to rounding
+            rtol = 1e-10 if cache.residual_tokens == 0 else 2e-5
+            np.testing.assert_allclose(w, c["weights"][g], rtol=rtol, atol=1e-15)
         o = pq.decode_attention(q, cache)
         peak_close(o, c["out"][g], OUT_RTOL_F32)
     np.testing.assert_array_equal(cache.values(), np.concatenate([c["values"], c["app_values"]]))
