@@ -120,11 +120,12 @@ def unit_bytes(T: int, G: int, d: int, m: int, n: int) -> int:
 # ------------------------------------------------------------- CPU baseline
 
 
-def _cpu_unit(args):
-    """Reference algorithm (numpy oracle port) for one unit: G query heads of
-    qk_scores + attention_weights + softmax.V.  Prefill is not timed (the GPU
-    step does not prefill either)."""
-    T, d, m, n, G, seed = args
+def _cpu_worker(args):
+    """One host core: build one (sequence, kv-head) unit with the reference
+    algorithm (numpy oracle port: prefill untimed -- the GPU step does not
+    prefill either), then repeat its decode -- G query heads of qk_scores +
+    attention_weights + softmax.V -- until ``seconds`` elapse."""
+    T, d, m, n, G, seed, seconds = args
     from oracle import polar_oracle as po
 
     keys = po.synthetic_keys(T, d, seed=seed, outliers=(0, 1))
@@ -133,40 +134,39 @@ def _cpu_unit(args):
     q = rng.standard_normal((G, d)).astype(np.float32)
     oc = po.OracleCache(m, n, po.HALF_SPLIT, 0)
     oc.prefill(keys, vals)
-    t0 = time.perf_counter()
-    for g in range(G):
-        oc.attention(q[g], 1.0 / math.sqrt(d))
-    return time.perf_counter() - t0
+    done, t0 = 0, time.perf_counter()
+    while True:
+        for g in range(G):
+            oc.attention(q[g], 1.0 / math.sqrt(d))
+        done += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return done, el
 
 
 def cpu_baseline(T, d, m, n, G, units_per_step, batch, seconds: float) -> dict:
-    """Time the reference CPU path on every host core (process pool, one unit
-    per task) for ~``seconds`` and extrapolate linearly to a full decode step."""
+    """Reference CPU path on every host core (one process per core) for
+    ~``seconds`` of decode work each, extrapolated linearly to a full step."""
     from concurrent.futures import ProcessPoolExecutor
 
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     cores = len(os.sched_getaffinity(0))
-    # one probe to size the sample
-    probe = _cpu_unit((T, d, m, n, G, 10_000))
-    per_core = max(1, int(seconds / max(probe, 1e-3)))
-    tasks = [(T, d, m, n, G, 10_001 + i) for i in range(per_core * cores)]
     t0 = time.perf_counter()
     with ProcessPoolExecutor(max_workers=cores) as ex:
-        unit_times = list(ex.map(_cpu_unit, tasks))
+        res = list(ex.map(_cpu_worker, [(T, d, m, n, G, 10_001 + i, seconds) for i in range(cores)]))
     wall = time.perf_counter() - t0
-    # decode work only (the sample also generated + prefilled each unit):
-    busy = sum(unit_times)
-    units_per_s = len(tasks) / (busy / cores)
+    units_per_s = sum(k / el for k, el in res)
     step_s = units_per_step / units_per_s
+    n_units = sum(k for k, _ in res)
     return {
         "value": batch / step_s,
         "unit": "tokens/s",
         "cores": cores,
         "kind": "port",
-        "sample": f"{len(tasks)} units x {G} query heads @ T={T} (qk_scores+attention_weights+softmax.V, numpy "
-                  f"oracle port of the reference), {cores} processes, {wall:.1f}s wall; extrapolated linearly to "
-                  f"{units_per_step} units/step",
-        "sec_per_unit_1core": busy / len(tasks),
+        "sample": f"{n_units} unit-decodes ({G} query heads each, T={T}: qk_scores + attention_weights + "
+                  f"softmax.V of the numpy oracle port of the reference) on {cores} processes, {wall:.1f}s wall "
+                  f"incl. setup; rate extrapolated linearly to {units_per_step} units/step",
+        "sec_per_unit_1core": cores / units_per_s,
     }
 
 

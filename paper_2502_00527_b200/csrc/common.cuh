@@ -64,6 +64,17 @@ PQB_DEV float load1(const void* base, int64_t elem_off) {
 
 PQB_DEV float half_bits_to_f32(uint16_t h) { return __half2float(__ushort_as_half(h)); }
 
+// Byte offset of value element (token t of a page, dim e) inside the page's
+// value region.  bf16 rows of d = 128 (256 B) are stored with their 16-byte
+// chunks XOR-swizzled by (t & 7): a linear bulk copy of a tile then lands in
+// shared memory in the conflict-free layout ldmatrix.trans needs (8 rows of the
+// same logical chunk hit 8 different bank groups).  Other shapes are linear.
+PQB_DEV int64_t value_offset(int64_t t, int e, int d, int value_dtype) {
+  if (value_dtype == PQB_F32) return (t * d + e) * 4;
+  if (d == 128) return t * 256 + ((((e >> 3) ^ static_cast<int>(t & 7))) << 4) + ((e & 7) << 1);
+  return (t * d + e) * 2;
+}
+
 // ---------------------------------------------------------------- warp ops
 
 PQB_DEV float warp_max(float v) {

@@ -1,24 +1,32 @@
 // HP-2: fused LUT decode attention (sm_100a).
 //
-//   reference  build_angle_table / build_query_lut   lut_decode.py:63-104
+//   reference  build_angle_table / build_query_lut    lut_decode.py:63-104
 //              qk_scores (LUT gather x dequantized radius) lut_decode.py:119-154
-//              _residual_scores (exact fp32 dots)     lut_decode.py:107-116
-//              attention_weights (softmax)            lut_decode.py:189-206
-//              softmax . V  -- not in the reference; restated over values() (kv_cache.py:247-259)
+//              _residual_scores (exact fp32 dots)      lut_decode.py:107-116
+//              attention_weights (softmax)             lut_decode.py:189-206
+//              softmax . V -- not in the reference; restated over values() (kv_cache.py:247-259)
 //
-// One CTA = one (unit, split) pair: a unit is one (layer, sequence, kv head)
-// with G query heads (GQA).  The CTA builds the unit's query lookup table
-//   P[j][a][g] = fl(fl(qx_gj * cos_a) + fl(qy_gj * sin_a))       (fp32, in smem)
-// and the radius table rhat[j][r] = fl(s_j * r), then 8 warps stream 32-token
-// tiles of the paged cache.  Each warp owns a private 2-stage ring in shared
-// memory fed by the TMA bulk-copy engine (cp.async.bulk + mbarrier complete_tx):
-// per tile the angle codes (32*8m B), radius codes (32*8n B) and values (8 KB bf16).
-//   scoring  lane = token: acc_g = fl(acc_g + fl(P[j][A_j][g] * rhat[j][R_j])) over
-//            j = 0..63 in order -- the reference's exact float32 operation sequence,
-//            so quantized-token scores are bit-identical to qk_scores.
-//   softmax  warp-level online softmax (tile max via shuffles, exp2).
-//   P.V      lane = 4 value dims: o[g][:] += p_g(t) * V[t][:] over the tile.
-// Warps merge in shared memory; splits merge in a small LSE-combine kernel.
+// decode_fast_kernel<G, M, N, EXACT>  (d = 128, bf16 values; the hot kernel)
+//   Persistent: one CTA per SM walks a balanced range of (unit, 32-token tile)
+//   work items; a unit is one (layer, sequence, kv head) with G query heads.
+//   Per unit segment the CTA builds the query lookup table in shared memory,
+//       P[j][a][g] = fl(fl(qx_gj * cos_a) + fl(qy_gj * sin_a))      (lut_decode.py:97-104)
+//   stored as float2 planes [j][g/2][a] (128-B rows: LDS.64 gathers are bank-
+//   conflict free for any code pattern).  8 warps each own a private 2-stage ring
+//   fed by the TMA bulk-copy engine (cp.async.bulk + mbarrier complete_tx): per
+//   tile the angle codes, radius codes and the 8 KB bf16 value tile.
+//   * scoring, lane = token.  Codes are masked into byte lanes once per word and
+//     picked with one PRMT each; the radius becomes a float with PRMT + FADD
+//     (magic 2^23).  EXACT: acc = fl(acc + fl(P * rhat)) in channel order -- the
+//     reference's fp32 op sequence, bit-identical scores (qk_scores mode).
+//     Fast (fused attention): LUT pre-scaled by s_j, acc = fma(P*s_j, r, acc).
+//   * softmax: warp-level online softmax (tile max by shuffles, exp2).
+//   * P.V on tensor cores: O^T[128 x 8] += V^T[128 x 32] . P^T[32 x 8] with
+//     mma.sync m16n8k16 (bf16 in, fp32 accumulate).  V^T fragments come straight
+//     from the tile with ldmatrix.trans (the page stores value rows XOR-swizzled,
+//     value_offset(), so the 8 rows of a fragment hit 8 bank groups); P is split
+//     into bf16 hi + lo (p - hi) so the product keeps ~2^-17 relative accuracy.
+//   Segment partials (m, l, o) are LSE-merged by combine_split_kernel.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -31,6 +39,7 @@ constexpr int kStages = 2;  // TMA ring depth per warp
 constexpr int kTile = 32;   // tokens per tile (one per lane)
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr double kPiD = 3.141592653589793115997963468544185161590576171875;  // == np.pi
+constexpr uint32_t kMagic = 0x4B000000u;  // 2^23 as float bits
 
 PQB_DEV const uint8_t* page_base_c(const pqb_store& s, int64_t unit, int64_t page) {
   const int64_t pid = s.page_table ? static_cast<int64_t>(__ldg(s.page_table + unit * s.max_pages + page))
@@ -46,49 +55,86 @@ PQB_DEV void angle_unit(int m, int a, float& c, float& s) {
   s = __double2float_rn(sin(g));
 }
 
-template <int DT>
-PQB_DEV float ldq(const void* q, int64_t i) { return load1<DT>(q, i); }
-
 PQB_DEV float load_q(const void* q, int dt, int64_t i) {
-  return dt == PQB_F32 ? ldq<PQB_F32>(q, i) : (dt == PQB_BF16 ? ldq<PQB_BF16>(q, i) : ldq<PQB_F16>(q, i));
+  return dt == PQB_F32 ? load1<PQB_F32>(q, i) : (dt == PQB_BF16 ? load1<PQB_BF16>(q, i) : load1<PQB_F16>(q, i));
 }
 
-// code j of a token whose 64*B code bits are in w[] (little-endian stream bits)
-template <int B>
-PQB_DEV uint32_t code_at(const uint32_t* w, int j) {
-  const int bit = j * B, wi = bit >> 5, sh = bit & 31;
-  uint32_t v;
-  if (sh + B <= 32) v = w[wi] >> sh;
-  else v = __funnelshift_r(w[wi], w[wi + 1], sh);
-  return v & ((1u << B) - 1u);
-}
+PQB_DEV uint32_t shift_lr(uint32_t x, int s) { return s >= 0 ? (x >> s) : (x << (-s)); }
 
-template <int G>
-PQB_DEV void lds_g(const float* p, float (&v)[G]) {
-  if constexpr (G == 1) {
-    v[0] = p[0];
-  } else if constexpr (G == 2) {
-    const float2 t = *reinterpret_cast<const float2*>(p);
-    v[0] = t.x; v[1] = t.y;
-  } else {
+// ---- code extraction.  A token's 64 codes of B bits are 2B words (stream
+// bits, LSB first).  For B in {2, 4} the codes are first masked into byte lanes
+// (scaled by 2^S); afterwards each code is one PRMT.
+
+template <int B, int S>
+struct CodeLanes {
+  static constexpr int kMasked = (B == 4 || B == 2) ? 16 : 1;
+  uint32_t mw[kMasked];
+  PQB_DEV void init(const uint32_t* w) {
+    if constexpr (B == 4) {
 #pragma unroll
-    for (int i = 0; i < G; i += 4) {
-      const float4 t = *reinterpret_cast<const float4*>(p + i);
-      v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
+      for (int i = 0; i < 8; ++i) {
+        mw[2 * i] = shift_lr(w[i], -S) & (0x0F0F0F0Fu << S);         // even codes: byte k = code 2k
+        mw[2 * i + 1] = shift_lr(w[i], 4 - S) & (0x0F0F0F0Fu << S);  // odd codes
+      }
+    } else if constexpr (B == 2) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) mw[4 * i + r] = shift_lr(w[i], 2 * r - S) & (0x03030303u << S);
     }
   }
+  // code j << S, as a register usable as an address offset
+  PQB_DEV uint32_t get(const uint32_t* w, int j) const {
+    if constexpr (B == 4) {
+      return __byte_perm(mw[2 * (j >> 3) + (j & 1)], 0u, 0x4440u | ((j & 7) >> 1));
+    } else if constexpr (B == 2) {
+      return __byte_perm(mw[4 * (j >> 4) + (j & 3)], 0u, 0x4440u | ((j & 15) >> 2));
+    } else {
+      const int bit = j * B, wi = bit >> 5, sh = bit & 31;
+      uint32_t v;
+      if (sh + B <= 32) v = shift_lr(w[wi], sh - S);
+      else v = __funnelshift_r(w[wi], w[wi + 1], sh) << S;
+      return v & (((1u << B) - 1u) << S);
+    }
+  }
+  // float(code j), exact (requires S == 0)
+  PQB_DEV float as_float(const uint32_t* w, int j) const {
+    uint32_t bits;
+    if constexpr (B == 4) {
+      bits = __byte_perm(mw[2 * (j >> 3) + (j & 1)], kMagic, 0x7650u | ((j & 7) >> 1));
+    } else if constexpr (B == 2) {
+      bits = __byte_perm(mw[4 * (j >> 4) + (j & 3)], kMagic, 0x7650u | ((j & 15) >> 2));
+    } else {
+      bits = get(w, j) | kMagic;
+    }
+    return __uint_as_float(bits) - 8388608.0f;
+  }
+};
+
+// ---- tensor-core helpers
+
+PQB_DEV void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+PQB_DEV void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
 // ------------------------------------------------------------------ epilogue
-// Merge the NW warps' (m, l, o) states of one CTA; o element (g, k) of lane L is
-// value dim dim_of(L, k).  Writes either the normalized output (single split) or
-// the split's partial state.
+
 struct EpiArgs {
   void* out;
   int out_dtype;
-  float* part_ml;  // [n_units][n_splits][G][2]
-  float* part_o;   // [n_units][n_splits][G][d]
-  int n_splits;
+  float* part_ml;  // [n_units][slots][G][2]
+  float* part_o;   // [n_units][slots][G][d]
+  int slots;       // partial slots per unit
 };
 
 PQB_DEV void store_out(void* out, int dt, int64_t idx, float v) {
@@ -96,226 +142,373 @@ PQB_DEV void store_out(void* out, int dt, int64_t idx, float v) {
   else static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
 }
 
-// ------------------------------------------------------------------ fast kernel
-
-template <int G, int M, int N>
-struct FastCfg {
-  static constexpr int kLutFloats = 64 * (1 << M) * G;
-  static constexpr int kRtabFloats = 64 * (1 << N);
-  static constexpr int kABytes = kTile * 8 * M;
-  static constexpr int kRBytes = kTile * 8 * N;
-  static constexpr int kVBytes = kTile * 128 * 2;
-  static constexpr int kStageBytes = kABytes + kRBytes + kVBytes;
-  static constexpr int kHeadBytes = (kLutFloats + kRtabFloats + G * 128 + 64) * 4;
-  static constexpr int kWarpBytes = kStages * kStageBytes + kTile * G * 4 + 64;
-  static constexpr int kSmem = kHeadBytes + kNW * kWarpBytes + 128;
+// Persistent work split: items = n_units * tiles_max, CTA c owns
+// [c*per_cta, min(items, (c+1)*per_cta)).  The slot of (unit u, CTA c) is
+// c - first_cta(u).
+struct WorkSplit {
+  int64_t items, per_cta;
+  int tiles_max;
 };
 
-template <int G, int M, int N>
+PQB_DEV int64_t first_cta(const WorkSplit& w, int64_t unit) { return (unit * w.tiles_max) / w.per_cta; }
+
+// ------------------------------------------------------------------ fast kernel
+
+template <int G, int M, int N, bool EXACT>
+struct FastCfg {
+  static constexpr int GP = G >= 2 ? G / 2 : 1;  // float2 planes
+  static constexpr int kS = G >= 2 ? 3 : 2;      // log2(LUT entry bytes)
+  static constexpr int kLutFloats = 64 * (1 << M) * G;
+  static constexpr int kRtabFloats = EXACT ? 64 * (1 << N) : 0;
+  static constexpr int kABytes = kTile * 8 * M;
+  static constexpr int kRBytes = kTile * 8 * N;
+  static constexpr int kVBytes = kTile * 256;
+  static constexpr int kStageBytes = kABytes + kRBytes + kVBytes;
+  static constexpr int kPBytes = 2 * 8 * kTile * 2;  // bf16 [hi/lo][8 queries][32 tokens]
+  static constexpr int kHeadBytes = (kLutFloats + kRtabFloats + G * 128 + 64) * 4;
+  static constexpr int kWarpBytes = kStages * kStageBytes + kPBytes + 64;
+  static constexpr int kSmem = kHeadBytes + kNW * kWarpBytes + 128;
+  static_assert(kHeadBytes % 16 == 0 && kWarpBytes % 16 == 0, "alignment");
+  static_assert(kNW * kStages * kStageBytes >= kNW * G * 132 * 4, "merge area");
+};
+
+template <int G, int M, int N, bool EXACT>
 __global__ void __launch_bounds__(kNW * 32, 1)
     decode_fast_kernel(const pqb_cache c, const void* __restrict__ q, int q_dtype, float sm_scale_log2,
-                       float* __restrict__ scores, int64_t scores_ld, EpiArgs ep, int tiles_per_split) {
-  using Cfg = FastCfg<G, M, N>;
+                       float* __restrict__ scores, int64_t scores_ld, EpiArgs ep, WorkSplit ws) {
+  using Cfg = FastCfg<G, M, N, EXACT>;
+  constexpr int GP = Cfg::GP;
   extern __shared__ __align__(128) uint8_t smem[];
-  float* lut = reinterpret_cast<float*>(smem);             // [64][2^M][G]
-  float* rtab = lut + Cfg::kLutFloats;                      // [64][2^N]
-  float* q_s = rtab + Cfg::kRtabFloats;                     // [G][128]
-  float* cs_s = q_s + G * 128;                              // cos[16] | sin[16] | spare
+  float* lut = reinterpret_cast<float*>(smem);  // [64][GP][2^M][2] (G>=2) or [64][2^M]
+  float* rtab = lut + Cfg::kLutFloats;           // EXACT: [64][2^N]
+  float* q_s = rtab + Cfg::kRtabFloats;          // [G][128]
+  float* cs_s = q_s + G * 128;                   // cos[16] | sin[16] | spare
   uint8_t* warp_area = smem + Cfg::kHeadBytes;
+  const uint8_t* lut_b = reinterpret_cast<const uint8_t*>(lut);
+  const uint8_t* rtab_b = reinterpret_cast<const uint8_t*>(rtab);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t unit = blockIdx.y;
-  const int split = blockIdx.x;
-  const int T = c.seq_lens[unit], Tq = c.quant_lens[unit];
-  const int n_tiles = (T + kTile - 1) / kTile;
-  const int tile_lo = split * tiles_per_split;
-  const int tile_hi = min(n_tiles, tile_lo + tiles_per_split);
   const bool want_out = ep.out != nullptr;
-
   uint8_t* my_area = warp_area + warp * Cfg::kWarpBytes;
-  float* pbuf = reinterpret_cast<float*>(my_area + kStages * Cfg::kStageBytes);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(my_area + kStages * Cfg::kStageBytes + kTile * G * 4);
-
-  // ---- per-CTA setup: query rows, angle/radius tables, LUT, barriers
-  for (int i = tid; i < G * 128; i += blockDim.x) q_s[i] = load_q(q, q_dtype, unit * G * 128 + i);
-  if (tid < (1 << M)) angle_unit(M, tid, cs_s[tid], cs_s[16 + tid]);
-  for (int i = tid; i < Cfg::kRtabFloats; i += blockDim.x) {
-    const int j = i >> N, r = i & ((1 << N) - 1);
-    rtab[i] = __fmul_rn(half_bits_to_f32(c.scales[unit * 64 + j]), static_cast<float>(r));
-  }
+  uint8_t* pbuf = my_area + kStages * Cfg::kStageBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(pbuf + Cfg::kPBytes);
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(bar + s, 1);
     fence_mbar_init();
   }
-  __syncthreads();
-  for (int i = tid; i < Cfg::kLutFloats; i += blockDim.x) {
-    const int g = i % G, a = (i / G) & ((1 << M) - 1), j = i / (G * (1 << M));
-    const int ex = c.layout == PQB_HALF_SPLIT ? j : 2 * j;
-    const int ey = c.layout == PQB_HALF_SPLIT ? j + 64 : 2 * j + 1;
-    lut[i] = __fadd_rn(__fmul_rn(q_s[g * 128 + ex], cs_s[a]), __fmul_rn(q_s[g * 128 + ey], cs_s[16 + a]));
-  }
-  __syncthreads();
-
-  // ---- TMA producer (lane 0 of each warp feeds its own ring)
   const int64_t P = c.store.page_tokens;
-  auto issue = [&](int tile, int s) {
-    uint8_t* st = my_area + s * Cfg::kStageBytes;
-    const int64_t tok0 = static_cast<int64_t>(tile) * kTile;
-    const int64_t page = tok0 / P, in_page = tok0 - page * P;
-    const uint8_t* pb = page_base_c(c.store, unit, page);
-    const uint32_t bytes = Cfg::kABytes + Cfg::kRBytes + (want_out ? Cfg::kVBytes : 0);
-    mbar_arrive_expect_tx(bar + s, bytes);
-    bulk_g2s(st, pb + c.store.angle_off + in_page * 8 * M, Cfg::kABytes, bar + s);
-    bulk_g2s(st + Cfg::kABytes, pb + c.store.radius_off + in_page * 8 * N, Cfg::kRBytes, bar + s);
-    if (want_out) bulk_g2s(st + Cfg::kABytes + Cfg::kRBytes, pb + c.store.value_off + in_page * 256, Cfg::kVBytes,
-                           bar + s);
-  };
-  const int first = tile_lo + warp;
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < kStages; ++s)
-      if (first + s * kNW < tile_hi) issue(first + s * kNW, s);
-  }
-  __syncwarp();
+  const int64_t i_begin = static_cast<int64_t>(blockIdx.x) * ws.per_cta;
+  const int64_t i_end = min(ws.items, i_begin + ws.per_cta);
+  uint32_t k_iter = 0;  // per-warp ring position, continues across segments
 
-  float m_run[G], l_run[G], o[G][4];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    m_run[g] = -INFINITY;
-    l_run[g] = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) o[g][k] = 0.0f;
-  }
+  // lane constants for the tensor-core P.V
+  const int qn = lane >> 2, t4 = lane & 3;  // fragment query column / pair
+  const uint32_t ld_row = static_cast<uint32_t>((((lane >> 4) & 1) * 8 + (lane & 7)) * 256);
+  const uint32_t ld_chunk = static_cast<uint32_t>((((lane >> 3) & 1) ^ (lane & 7)) << 4);
 
-  int k_iter = 0;
-  for (int tile = first; tile < tile_hi; tile += kNW, ++k_iter) {
-    const int s = k_iter % kStages;
-    mbar_wait(bar + s, (k_iter / kStages) & 1);
-    const uint8_t* st = my_area + s * Cfg::kStageBytes;
-    const int tok = tile * kTile + lane;
-    float acc[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) acc[g] = 0.0f;
-    if (tok < Tq) {
-      uint32_t wa[2 * M + 1], wr[2 * N + 1];
-      const uint2* pa = reinterpret_cast<const uint2*>(st + lane * 8 * M);
-      const uint2* pr = reinterpret_cast<const uint2*>(st + Cfg::kABytes + lane * 8 * N);
-#pragma unroll
-      for (int i = 0; i < M; ++i) { const uint2 v = pa[i]; wa[2 * i] = v.x; wa[2 * i + 1] = v.y; }
-#pragma unroll
-      for (int i = 0; i < N; ++i) { const uint2 v = pr[i]; wr[2 * i] = v.x; wr[2 * i + 1] = v.y; }
-      wa[2 * M] = 0u;
-      wr[2 * N] = 0u;
-#pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        const uint32_t a = code_at<M>(wa, j), r = code_at<N>(wr, j);
-        const float rh = rtab[j * (1 << N) + r];
-        float pv[G];
-        lds_g<G>(lut + (j * (1 << M) + a) * G, pv);
-#pragma unroll
-        for (int g = 0; g < G; ++g) acc[g] = __fadd_rn(acc[g], __fmul_rn(pv[g], rh));
-      }
-    } else if (tok < T) {  // residual window: exact fp32 dot (lut_decode.py:107-116)
-      const float* kr = c.residual + (unit * c.res_cap + tok % c.res_cap) * 128;
-      for (int e = 0; e < 128; ++e) {
-        const float kv = kr[e];
-#pragma unroll
-        for (int g = 0; g < G; ++g) acc[g] = fmaf(kv, q_s[g * 128 + e], acc[g]);
+  for (int64_t seg = i_begin; seg < i_end;) {
+    const int64_t unit = seg / ws.tiles_max;
+    const int t_lo = static_cast<int>(seg - unit * ws.tiles_max);
+    const int64_t seg_end = min(i_end, (unit + 1) * ws.tiles_max);
+    seg = seg_end;
+    const int T = c.seq_lens[unit], Tq = c.quant_lens[unit];
+    const int n_tiles = (T + kTile - 1) / kTile;
+    const int t_hi = min(static_cast<int>(seg_end - unit * ws.tiles_max), n_tiles);
+
+    // ---- unit setup: query rows, angle table, LUT (+ radius table)
+    __syncthreads();  // previous segment finished with LUT / merge area
+    for (int i = tid; i < G * 128; i += blockDim.x) q_s[i] = load_q(q, q_dtype, unit * G * 128 + i);
+    if (tid < (1 << M)) angle_unit(M, tid, cs_s[tid], cs_s[16 + tid]);
+    if constexpr (EXACT) {
+      for (int i = tid; i < Cfg::kRtabFloats; i += blockDim.x) {
+        const int j = i >> N, r = i & ((1 << N) - 1);
+        rtab[i] = __fmul_rn(half_bits_to_f32(c.scales[unit * 64 + j]), static_cast<float>(r));
       }
     }
-    if (scores != nullptr && tok < T) {
-#pragma unroll
-      for (int g = 0; g < G; ++g) scores[(unit * G + g) * scores_ld + tok] = acc[g];
-    }
-    if (want_out) {
-      float alpha[G], p[G];
-#pragma unroll
-      for (int g = 0; g < G; ++g) {
-        const float x = tok < T ? acc[g] * sm_scale_log2 : -INFINITY;
-        const float mt = warp_max(x);
-        const float mn = fmaxf(m_run[g], mt);
-        alpha[g] = exp2f(m_run[g] - mn);
-        p[g] = exp2f(x - mn);
-        l_run[g] = fmaf(l_run[g], alpha[g], p[g]);
-        m_run[g] = mn;
+    __syncthreads();
+    for (int i = tid; i < Cfg::kLutFloats; i += blockDim.x) {
+      // i = ((j*GP + gp) * 2^M + a) * 2 + h   (G >= 2)   |   j * 2^M + a   (G == 1)
+      int j, a, g;
+      if constexpr (G >= 2) {
+        const int h = i & 1, rest = i >> 1;
+        a = rest & ((1 << M) - 1);
+        const int jg = rest >> M;
+        j = jg / GP;
+        g = (jg % GP) * 2 + h;
+      } else {
+        a = i & ((1 << M) - 1);
+        j = i >> M;
+        g = 0;
       }
+      const int ex = c.layout == PQB_HALF_SPLIT ? j : 2 * j;
+      const int ey = c.layout == PQB_HALF_SPLIT ? j + 64 : 2 * j + 1;
+      float v = __fadd_rn(__fmul_rn(q_s[g * 128 + ex], cs_s[a]), __fmul_rn(q_s[g * 128 + ey], cs_s[16 + a]));
+      if constexpr (!EXACT) v = __fmul_rn(v, half_bits_to_f32(c.scales[unit * 64 + j]));
+      lut[i] = v;
+    }
+    __syncthreads();
+
+    // ---- TMA producer: lane 0 of each warp feeds its own ring
+    auto issue = [&](int tile, uint32_t s) {
+      uint8_t* st = my_area + s * Cfg::kStageBytes;
+      const int64_t tok0 = static_cast<int64_t>(tile) * kTile;
+      const int64_t page = tok0 / P, in_page = tok0 - page * P;
+      const uint8_t* pb = page_base_c(c.store, unit, page);
+      const uint32_t bytes = Cfg::kABytes + Cfg::kRBytes + (want_out ? Cfg::kVBytes : 0);
+      mbar_arrive_expect_tx(bar + s, bytes);
+      bulk_g2s(st, pb + c.store.angle_off + in_page * 8 * M, Cfg::kABytes, bar + s);
+      bulk_g2s(st + Cfg::kABytes, pb + c.store.radius_off + in_page * 8 * N, Cfg::kRBytes, bar + s);
+      if (want_out)
+        bulk_g2s(st + Cfg::kABytes + Cfg::kRBytes, pb + c.store.value_off + in_page * 256, Cfg::kVBytes, bar + s);
+    };
+    const int first = t_lo + warp;
+    if (lane == 0) {
 #pragma unroll
-      for (int g = 0; g < G; ++g) pbuf[lane * G + g] = p[g];
-      __syncwarp();
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-#pragma unroll
-        for (int k = 0; k < 4; ++k) o[g][k] *= alpha[g];
-      const int nvalid = min(kTile, T - tile * kTile);
-      const uint8_t* vs = st + Cfg::kABytes + Cfg::kRBytes;
-#pragma unroll 4
-      for (int t = 0; t < nvalid; ++t) {
-        const uint2 vv = *reinterpret_cast<const uint2*>(vs + t * 256 + lane * 8);
-        const float v0 = __uint_as_float(vv.x << 16), v1 = __uint_as_float(vv.x & 0xffff0000u);
-        const float v2 = __uint_as_float(vv.y << 16), v3 = __uint_as_float(vv.y & 0xffff0000u);
-        float pt[G];
-        lds_g<G>(pbuf + t * G, pt);
-#pragma unroll
-        for (int g = 0; g < G; ++g) {
-          o[g][0] = fmaf(pt[g], v0, o[g][0]);
-          o[g][1] = fmaf(pt[g], v1, o[g][1]);
-          o[g][2] = fmaf(pt[g], v2, o[g][2]);
-          o[g][3] = fmaf(pt[g], v3, o[g][3]);
+      for (int s = 0; s < kStages; ++s) {
+        const int tile = first + s * kNW;
+        if (tile < t_hi) {
+          fence_proxy_async_smem();
+          issue(tile, (k_iter + s) % kStages);
         }
       }
     }
     __syncwarp();
+
+    float m_run[G], l_run[G];
+    float d[8][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      m_run[g] = -INFINITY;
+      l_run[g] = 0.0f;
+    }
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d[mt][k] = 0.0f;
+
+    for (int tile = first; tile < t_hi; tile += kNW, ++k_iter) {
+      const uint32_t s = k_iter % kStages;
+      mbar_wait(bar + s, (k_iter / kStages) & 1);
+      const uint8_t* st = my_area + s * Cfg::kStageBytes;
+      const int tok = tile * kTile + lane;
+      float acc[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[g] = 0.0f;
+      if (tok < Tq) {
+        uint32_t wa[2 * M + 1], wr[2 * N + 1];
+        const uint2* pa = reinterpret_cast<const uint2*>(st + lane * 8 * M);
+        const uint2* pr = reinterpret_cast<const uint2*>(st + Cfg::kABytes + lane * 8 * N);
+#pragma unroll
+        for (int i = 0; i < M; ++i) { const uint2 v = pa[i]; wa[2 * i] = v.x; wa[2 * i + 1] = v.y; }
+#pragma unroll
+        for (int i = 0; i < N; ++i) { const uint2 v = pr[i]; wr[2 * i] = v.x; wr[2 * i + 1] = v.y; }
+        wa[2 * M] = 0u;
+        wr[2 * N] = 0u;
+        CodeLanes<M, Cfg::kS> ca;
+        ca.init(wa);
+        if constexpr (EXACT) {
+          CodeLanes<N, 2> cr;
+          cr.init(wr);
+#pragma unroll
+          for (int j = 0; j < 64; ++j) {
+            const uint32_t aoff = ca.get(wa, j);
+            const float rh = *reinterpret_cast<const float*>(rtab_b + (j << (N + 2)) + cr.get(wr, j));
+            float pv[G];
+            if constexpr (G >= 2) {
+#pragma unroll
+              for (int gp = 0; gp < GP; ++gp) {
+                const float2 t = *reinterpret_cast<const float2*>(lut_b + (((j * GP + gp) << M) << 3) + aoff);
+                pv[2 * gp] = t.x;
+                pv[2 * gp + 1] = t.y;
+              }
+            } else {
+              pv[0] = *reinterpret_cast<const float*>(lut_b + ((j << M) << 2) + aoff);
+            }
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[g] = __fadd_rn(acc[g], __fmul_rn(pv[g], rh));
+          }
+        } else {
+          CodeLanes<N, 0> cr;
+          cr.init(wr);
+#pragma unroll
+          for (int j = 0; j < 64; ++j) {
+            const uint32_t aoff = ca.get(wa, j);
+            const float rf = cr.as_float(wr, j);
+            if constexpr (G >= 2) {
+#pragma unroll
+              for (int gp = 0; gp < GP; ++gp) {
+                const float2 t = *reinterpret_cast<const float2*>(lut_b + (((j * GP + gp) << M) << 3) + aoff);
+                acc[2 * gp] = fmaf(t.x, rf, acc[2 * gp]);
+                acc[2 * gp + 1] = fmaf(t.y, rf, acc[2 * gp + 1]);
+              }
+            } else {
+              const float t = *reinterpret_cast<const float*>(lut_b + ((j << M) << 2) + aoff);
+              acc[0] = fmaf(t, rf, acc[0]);
+            }
+          }
+        }
+      } else if (tok < T) {  // residual window: fp32 dot (lut_decode.py:107-116)
+        const float* kr = c.residual + (unit * c.res_cap + tok % c.res_cap) * 128;
+        for (int e = 0; e < 128; ++e) {
+          const float kv = kr[e];
+#pragma unroll
+          for (int g = 0; g < G; ++g) acc[g] = fmaf(kv, q_s[g * 128 + e], acc[g]);
+        }
+      }
+      if (scores != nullptr && tok < T) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) scores[(unit * G + g) * scores_ld + tok] = acc[g];
+      }
+      if (want_out) {
+        // ---- online softmax (per query, warp-uniform running max)
+        float alpha[G];
+        bool rescale = false;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float x = tok < T ? acc[g] * sm_scale_log2 : -INFINITY;
+          const float mn = fmaxf(m_run[g], warp_max(x));
+          alpha[g] = exp2f(m_run[g] - mn);
+          rescale |= mn != m_run[g];
+          const float p = exp2f(x - mn);
+          l_run[g] = fmaf(l_run[g], alpha[g], p);
+          m_run[g] = mn;
+          const __nv_bfloat16 hi = __float2bfloat16_rn(p);
+          const __nv_bfloat16 lo = __float2bfloat16_rn(p - __bfloat162float(hi));
+          reinterpret_cast<__nv_bfloat16*>(pbuf)[g * kTile + lane] = hi;
+          reinterpret_cast<__nv_bfloat16*>(pbuf)[(8 + g) * kTile + lane] = lo;
+        }
+        if (rescale) {  // warp-uniform
+          float a0 = 1.0f, a1 = 1.0f;
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            if (g == 2 * t4) a0 = alpha[g];
+            if (g == 2 * t4 + 1) a1 = alpha[g];
+          }
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            d[mt][0] *= a0;
+            d[mt][1] *= a1;
+            d[mt][2] *= a0;
+            d[mt][3] *= a1;
+          }
+        }
+        __syncwarp();
+        // ---- P.V on tensor cores: B = P^T fragments (hi, lo) for 2 k-steps
+        uint32_t b[2][2][2];
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+#pragma unroll
+          for (int pl = 0; pl < 2; ++pl) {
+            if (qn < G) {
+              const uint32_t* row = reinterpret_cast<const uint32_t*>(pbuf + ((pl * 8 + qn) * kTile + 16 * ks) * 2);
+              b[ks][pl][0] = row[t4];
+              b[ks][pl][1] = row[t4 + 4];
+            } else {
+              b[ks][pl][0] = b[ks][pl][1] = 0u;
+            }
+          }
+        const uint32_t vbase = smem_u32(st + Cfg::kABytes + Cfg::kRBytes) + ld_row;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4_trans(vbase + ks * 16 * 256 + (ld_chunk ^ (mt << 5)), a0, a1, a2, a3);
+            mma_bf16(d[mt], a0, a1, a2, a3, b[ks][0][0], b[ks][0][1]);
+            mma_bf16(d[mt], a0, a1, a2, a3, b[ks][1][0], b[ks][1][1]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int nt = tile + kStages * kNW;
+        if (nt < t_hi) {
+          fence_proxy_async_smem();
+          issue(nt, s);
+        }
+      }
+    }
+    if (!want_out) continue;
+
+    // ---- merge the warps of this segment (stage memory is idle now)
+#pragma unroll
+    for (int g = 0; g < G; ++g) l_run[g] = warp_sum(l_run[g]);
+    __syncthreads();
+    float* red = reinterpret_cast<float*>(warp_area);  // [NW][G][132]: m, l, pad, o[128]
+    float* mine = red + warp * G * 132;
     if (lane == 0) {
-      const int nt = tile + kStages * kNW;
-      if (nt < tile_hi) {
-        fence_proxy_async_smem();
-        issue(nt, s);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        mine[g * 132] = m_run[g];
+        mine[g * 132 + 1] = l_run[g];
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt) {
+      const int dim = 16 * mt + qn;
+      if (2 * t4 < G) {
+        mine[(2 * t4) * 132 + 4 + dim] = d[mt][0];
+        mine[(2 * t4) * 132 + 4 + dim + 8] = d[mt][2];
+      }
+      if (2 * t4 + 1 < G) {
+        mine[(2 * t4 + 1) * 132 + 4 + dim] = d[mt][1];
+        mine[(2 * t4 + 1) * 132 + 4 + dim + 8] = d[mt][3];
+      }
+    }
+    __syncthreads();
+    const int64_t slot = (unit * ep.slots + (blockIdx.x - first_cta(ws, unit))) * G;
+    for (int i = tid; i < G * 128; i += blockDim.x) {
+      const int g = i >> 7, e = i & 127;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, red[(w * G + g) * 132]);
+      float L = 0.0f, O = 0.0f;
+      if (mx != -INFINITY) {
+#pragma unroll
+        for (int w = 0; w < kNW; ++w) {
+          const float* rw = red + (w * G + g) * 132;
+          const float sc = exp2f(rw[0] - mx);
+          L = fmaf(rw[1], sc, L);
+          O = fmaf(rw[4 + e], sc, O);
+        }
+      }
+      ep.part_o[(slot + g) * 128 + e] = O;
+      if (e == 0) {
+        ep.part_ml[2 * (slot + g)] = mx;
+        ep.part_ml[2 * (slot + g) + 1] = L;
       }
     }
   }
-  if (!want_out) return;
+}
 
-  // ---- merge warps (stage memory is free: every issued copy was consumed)
-#pragma unroll
-  for (int g = 0; g < G; ++g) l_run[g] = warp_sum(l_run[g]);
-  __syncthreads();
-  float* red = reinterpret_cast<float*>(warp_area);  // [NW][G][4 + 128]: m, l, pad, o
-  float* mine = red + warp * G * 132;
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    if (lane == 0) { mine[g * 132] = m_run[g]; mine[g * 132 + 1] = l_run[g]; }
-    *reinterpret_cast<float4*>(mine + g * 132 + 4 + 4 * lane) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
-  }
-  __syncthreads();
-  for (int i = tid; i < G * 128; i += blockDim.x) {
+// LSE merge of the per-(unit, CTA) partials of decode_fast_kernel.
+__global__ void combine_split_kernel(const float* __restrict__ part_ml, const float* __restrict__ part_o,
+                                     WorkSplit ws, int slots, int G, void* out, int out_dtype) {
+  const int64_t unit = blockIdx.x;
+  const int64_t c0 = first_cta(ws, unit);
+  const int64_t c1 = ((unit + 1) * ws.tiles_max - 1) / ws.per_cta;
+  const int n = static_cast<int>(c1 - c0 + 1);
+  for (int i = threadIdx.x; i < G * 128; i += blockDim.x) {
     const int g = i >> 7, e = i & 127;
     float mx = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, red[(w * G + g) * 132]);
+    for (int s = 0; s < n; ++s) mx = fmaxf(mx, part_ml[2 * ((unit * slots + s) * G + g)]);
     float L = 0.0f, O = 0.0f;
-    if (mx != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < kNW; ++w) {
-        const float* rw = red + (w * G + g) * 132;
-        const float sc = exp2f(rw[0] - mx);
-        L = fmaf(rw[1], sc, L);
-        O = fmaf(rw[4 + e], sc, O);
-      }
+    for (int s = 0; s < n; ++s) {
+      const int64_t sl = (unit * slots + s) * G + g;
+      const float ms = part_ml[2 * sl];
+      if (ms == -INFINITY) continue;
+      const float sc = exp2f(ms - mx);
+      L = fmaf(part_ml[2 * sl + 1], sc, L);
+      O = fmaf(part_o[sl * 128 + e], sc, O);
     }
-    if (ep.n_splits == 1) {
-      store_out(ep.out, ep.out_dtype, (unit * G + g) * 128 + e, O / L);
-    } else {
-      const int64_t slot = (unit * ep.n_splits + split) * G + g;
-      ep.part_o[slot * 128 + e] = O;
-      if (e == 0) { ep.part_ml[2 * slot] = mx; ep.part_ml[2 * slot + 1] = L; }
-    }
+    store_out(out, out_dtype, (unit * G + g) * 128 + e, O / L);
   }
 }
 
 // ------------------------------------------------------------------ generic kernel
 // Any even d <= 256, m/n in 1..8, G <= 8, V f32 or bf16; codes and values read
-// straight from global memory.  Same float32 scoring sequence as the fast kernel.
+// straight from global memory.  Exact fp32 scoring sequence (as EXACT above).
 
 constexpr int kGenMaxG = 8, kGenMaxDpl = 8;
 
@@ -352,10 +545,7 @@ __global__ void __launch_bounds__(256)
   __syncthreads();
   float* pbuf = pbuf_all + warp * kTile * G;
   const int dpl = (d + 31) / 32;
-  const int vb = c.store.value_dtype == PQB_F32 ? 4 : 2;
   const int64_t P = c.store.page_tokens;
-  const int64_t a_page_bytes = P * half * m / 8, r_page_bytes = P * half * n / 8;
-  (void)a_page_bytes; (void)r_page_bytes;
   float m_run[kGenMaxG], l_run[kGenMaxG], o[kGenMaxG][kGenMaxDpl];
   for (int g = 0; g < kGenMaxG; ++g) {
     m_run[g] = -INFINITY; l_run[g] = 0.0f;
@@ -409,12 +599,13 @@ __global__ void __launch_bounds__(256)
     for (int t = 0; t < nvalid; ++t) {
       const int64_t ta = static_cast<int64_t>(tile) * kTile + t;
       const int64_t page = ta / P, in_page = ta - page * P;
-      const uint8_t* vrow = page_base_c(c.store, unit, page) + c.store.value_off + in_page * d * vb;
+      const uint8_t* vreg = page_base_c(c.store, unit, page) + c.store.value_off;
       for (int k = 0; k < dpl; ++k) {
         const int e = lane + 32 * k;
         if (e < d) {
-          const float v = vb == 4 ? reinterpret_cast<const float*>(vrow)[e]
-                                  : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(vrow)[e]);
+          const uint8_t* vp = vreg + value_offset(in_page, e, d, c.store.value_dtype);
+          const float v = c.store.value_dtype == PQB_F32 ? *reinterpret_cast<const float*>(vp)
+                                                         : __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(vp));
           for (int g = 0; g < G; ++g) o[g][k] = fmaf(pbuf[t * G + g], v, o[g][k]);
         }
       }
@@ -445,17 +636,17 @@ __global__ void __launch_bounds__(256)
         O = fmaf(rw[2 + e], sc, O);
       }
     }
-    if (ep.n_splits == 1) {
+    if (ep.slots == 1) {
       store_out(ep.out, ep.out_dtype, (unit * G + g) * d + e, O / L);
     } else {
-      const int64_t slot = (unit * ep.n_splits + split) * G + g;
+      const int64_t slot = (unit * ep.slots + split) * G + g;
       ep.part_o[slot * d + e] = O;
       if (e == 0) { ep.part_ml[2 * slot] = mx; ep.part_ml[2 * slot + 1] = L; }
     }
   }
 }
 
-// LSE combine of split partials: out = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M)
+// LSE combine of generic-kernel split partials.
 __global__ void combine_kernel(const float* __restrict__ part_ml, const float* __restrict__ part_o, int n_splits,
                                int G, int d, void* out, int out_dtype) {
   const int64_t unit = blockIdx.x;
@@ -488,68 +679,125 @@ static int num_sms() {
   return sms;
 }
 
-static int max_splits(int max_tokens) {
-  const int tiles = (max_tokens + kTile - 1) / kTile;
-  return std::max(1, std::min(64, tiles / (2 * kNW)));
-}
+constexpr int kMaxCtas = 256;  // bound used to size the partial-slot workspace
+
+static int tiles_of(int max_tokens) { return (max_tokens + kTile - 1) / kTile; }
+
+// generic kernel: (unit, split) grid
+static int max_splits(int max_tokens) { return std::max(1, std::min(64, tiles_of(max_tokens) / (2 * kNW))); }
 
 static int choose_splits(int64_t n_units, int max_tokens) {
   const int64_t want = (2 * static_cast<int64_t>(num_sms()) + n_units - 1) / n_units;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, max_splits(max_tokens))));
 }
 
+// fast kernel: persistent split over units x tiles
+static WorkSplit make_split(int64_t n_units, int max_tokens, int ctas) {
+  WorkSplit w;
+  w.tiles_max = tiles_of(max_tokens);
+  w.items = n_units * w.tiles_max;
+  const int64_t c = std::max<int64_t>(1, std::min<int64_t>(ctas, w.items));
+  w.per_cta = (w.items + c - 1) / c;
+  return w;
+}
+
+static int fast_slots(int64_t n_units, int max_tokens) {
+  // CTAs touching one unit <= ceil(tiles_max / per_cta) + 1 with per_cta >= items / kMaxCtas
+  const int tm = tiles_of(max_tokens);
+  const int64_t per_min = std::max<int64_t>(1, (n_units * tm) / kMaxCtas);
+  return static_cast<int>(std::min<int64_t>(tm, (tm + per_min - 1) / per_min + 1));
+}
+
 int decode_splits(int64_t n_units, int max_tokens) { return choose_splits(n_units, max_tokens); }
 
 size_t decode_workspace_bytes(int64_t n_units, int group, int max_tokens, int d) {
-  const int s = max_splits(max_tokens);
+  const int s = std::max(max_splits(max_tokens), fast_slots(n_units, max_tokens));
   return static_cast<size_t>(n_units) * s * group * (2 + d) * sizeof(float) + 256;
 }
 
-template <int G, int M, int N>
-static int launch_fast(const DecodeArgs& a, const EpiArgs& ep, int splits, int tps, cudaStream_t s) {
-  using Cfg = FastCfg<G, M, N>;
+template <int G, int M, int N, bool EXACT>
+static int launch_fast(const DecodeArgs& a, cudaStream_t s) {
+  using Cfg = FastCfg<G, M, N, EXACT>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(decode_fast_kernel<G, M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(decode_fast_kernel<G, M, N, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg::kSmem) != cudaSuccess) {
       set_error("cudaFuncSetAttribute(smem=%d) failed", Cfg::kSmem);
       return PQB_ECUDA;
     }
     attr_set = true;
   }
-  dim3 grid(splits, static_cast<unsigned>(a.n_units));
-  decode_fast_kernel<G, M, N><<<grid, kNW * 32, Cfg::kSmem, s>>>(*a.cache, a.q, a.q_dtype, a.sm_scale * kLog2e,
-                                                                 a.scores, a.scores_ld, ep, tps);
+  const int ctas = a.splits > 0 ? std::min(a.splits, kMaxCtas) : std::min(num_sms(), kMaxCtas);
+  const WorkSplit ws = make_split(a.n_units, a.max_tokens, ctas);
+  const int grid = static_cast<int>((ws.items + ws.per_cta - 1) / ws.per_cta);
+  EpiArgs ep;
+  ep.out = a.out;
+  ep.out_dtype = a.out_dtype;
+  ep.slots = fast_slots(a.n_units, a.max_tokens);
+  ep.part_ml = static_cast<float*>(a.workspace);
+  ep.part_o = ep.part_ml + a.n_units * ep.slots * G * 2;
+  if (a.out != nullptr) {
+    const size_t need = static_cast<size_t>(a.n_units) * ep.slots * G * (2 + 128) * sizeof(float);
+    if (a.workspace == nullptr || a.workspace_bytes < need) {
+      set_error("decode workspace too small: need %zu bytes, got %zu", need, a.workspace_bytes);
+      return PQB_EINVAL;
+    }
+  }
+  decode_fast_kernel<G, M, N, EXACT><<<grid, kNW * 32, Cfg::kSmem, s>>>(
+      *a.cache, a.q, a.q_dtype, a.sm_scale * kLog2e, a.scores, a.scores_ld, ep, ws);
+  if (a.out != nullptr && !(a.flags & PQB_DECODE_NO_COMBINE))
+    combine_split_kernel<<<static_cast<unsigned>(a.n_units), 128, 0, s>>>(ep.part_ml, ep.part_o, ws, ep.slots, G,
+                                                                           a.out, a.out_dtype);
   return PQB_OK;
 }
 
-template <int G>
-static int dispatch_fast_mn(const DecodeArgs& a, const EpiArgs& ep, int splits, int tps, cudaStream_t s,
-                            bool& handled) {
+template <int G, bool EXACT>
+static int dispatch_fast_mn(const DecodeArgs& a, cudaStream_t s, bool& handled) {
   handled = true;
-  const int mn = a.cache->angle_bits * 10 + a.cache->radius_bits;
-  switch (mn) {
-    case 44: return launch_fast<G, 4, 4>(a, ep, splits, tps, s);
-    case 32: return launch_fast<G, 3, 2>(a, ep, splits, tps, s);
-    case 22: return launch_fast<G, 2, 2>(a, ep, splits, tps, s);
-    case 42: return launch_fast<G, 4, 2>(a, ep, splits, tps, s);
-    case 24: return launch_fast<G, 2, 4>(a, ep, splits, tps, s);
-    case 34: return launch_fast<G, 3, 4>(a, ep, splits, tps, s);
+  switch (a.cache->angle_bits * 10 + a.cache->radius_bits) {
+    case 44: return launch_fast<G, 4, 4, EXACT>(a, s);
+    case 32: return launch_fast<G, 3, 2, EXACT>(a, s);
+    case 22: return launch_fast<G, 2, 2, EXACT>(a, s);
+    case 42: return launch_fast<G, 4, 2, EXACT>(a, s);
+    case 24: return launch_fast<G, 2, 4, EXACT>(a, s);
+    case 34: return launch_fast<G, 3, 4, EXACT>(a, s);
     default: handled = false; return PQB_OK;
   }
 }
 
+template <bool EXACT>
+static int dispatch_fast(const DecodeArgs& a, cudaStream_t s, bool& handled) {
+  if (a.group == 4) return dispatch_fast_mn<4, EXACT>(a, s, handled);
+  if (a.group == 8) return dispatch_fast_mn<8, EXACT>(a, s, handled);
+  return dispatch_fast_mn<1, EXACT>(a, s, handled);
+}
+
 int launch_decode(const DecodeArgs& a, cudaStream_t s) {
   const pqb_cache& c = *a.cache;
+  const bool fast_ok = c.d == 128 && (a.out == nullptr || c.store.value_dtype == PQB_BF16) &&
+                       (a.group == 1 || a.group == 4 || a.group == 8) && c.store.page_tokens % kTile == 0 &&
+                       (c.store.angle_off % 16 == 0) && (c.store.radius_off % 16 == 0) &&
+                       (c.store.value_off % 16 == 0 || a.out == nullptr) && (c.store.page_bytes % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(c.store.pool) % 16 == 0);
+  bool handled = false;
+  if (fast_ok && !(a.flags & PQB_DECODE_FORCE_GENERIC)) {
+    // scores requested -> the bit-exact scoring sequence; fused-only -> FMA form
+    const int rc = a.scores != nullptr ? dispatch_fast<true>(a, s, handled) : dispatch_fast<false>(a, s, handled);
+    if (rc != PQB_OK) return rc;
+  }
+  if (handled) return PQB_OK;
+  if (c.d > 256 || a.group > kGenMaxG) {
+    set_error("decode: d=%d group=%d unsupported (d <= 256, group <= %d)", c.d, a.group, kGenMaxG);
+    return PQB_EUNSUPPORTED;
+  }
   const int splits = a.splits > 0 ? std::min(a.splits, max_splits(a.max_tokens)) : choose_splits(a.n_units, a.max_tokens);
-  const int tiles = (a.max_tokens + kTile - 1) / kTile;
-  const int tps = (tiles + splits - 1) / splits;
+  const int tps = (tiles_of(a.max_tokens) + splits - 1) / splits;
   EpiArgs ep;
   ep.out = a.out;
   ep.out_dtype = a.out_dtype;
-  ep.n_splits = splits;
+  ep.slots = splits;
   ep.part_ml = static_cast<float*>(a.workspace);
-  ep.part_o = ep.part_ml + static_cast<int64_t>(a.n_units) * splits * a.group * 2;
+  ep.part_o = ep.part_ml + a.n_units * splits * a.group * 2;
   if (splits > 1 && a.out != nullptr) {
     const size_t need = static_cast<size_t>(a.n_units) * splits * a.group * (2 + c.d) * sizeof(float);
     if (a.workspace == nullptr || a.workspace_bytes < need) {
@@ -557,39 +805,19 @@ int launch_decode(const DecodeArgs& a, cudaStream_t s) {
       return PQB_EINVAL;
     }
   }
-  const bool fast_ok = c.d == 128 && (a.out == nullptr || c.store.value_dtype == PQB_BF16) &&
-                       (a.group == 1 || a.group == 4 || a.group == 8) && c.store.page_tokens % kTile == 0 &&
-                       (c.store.angle_off % 16 == 0) && (c.store.radius_off % 16 == 0) &&
-                       (c.store.value_off % 16 == 0 || a.out == nullptr) && (c.store.page_bytes % 16 == 0) &&
-                       (reinterpret_cast<uintptr_t>(c.store.pool) % 16 == 0);
-  int rc = PQB_OK;
-  bool handled = false;
-  if (fast_ok && !(a.flags & PQB_DECODE_FORCE_GENERIC)) {
-    if (a.group == 4) rc = dispatch_fast_mn<4>(a, ep, splits, tps, s, handled);
-    else if (a.group == 8) rc = dispatch_fast_mn<8>(a, ep, splits, tps, s, handled);
-    else rc = dispatch_fast_mn<1>(a, ep, splits, tps, s, handled);
-    if (rc != PQB_OK) return rc;
+  const size_t shm = sizeof(float) * (a.group * c.d + 512 + c.d / 2 + kNW * kTile * a.group +
+                                      kNW * a.group * (2 + c.d));
+  static size_t attr = 0;
+  if (shm > 48 * 1024 && shm > attr) {
+    cudaFuncSetAttribute(decode_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
+    attr = shm;
   }
-  if (!handled) {
-    if (c.d > 256 || a.group > kGenMaxG) {
-      set_error("decode: d=%d group=%d unsupported (d <= 256, group <= %d)", c.d, a.group, kGenMaxG);
-      return PQB_EUNSUPPORTED;
-    }
-    const size_t shm = sizeof(float) * (a.group * c.d + 512 + c.d / 2 + kNW * kTile * a.group +
-                                        kNW * a.group * (2 + c.d));
-    static size_t attr = 0;
-    if (shm > 48 * 1024 && shm > attr) {
-      cudaFuncSetAttribute(decode_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
-      attr = shm;
-    }
-    dim3 grid(splits, static_cast<unsigned>(a.n_units));
-    decode_generic_kernel<<<grid, kNW * 32, shm, s>>>(c, a.group, a.q, a.q_dtype, a.sm_scale * kLog2e, a.scores,
-                                                      a.scores_ld, ep, tps);
-  }
-  if (splits > 1 && a.out != nullptr && !(a.flags & PQB_DECODE_NO_COMBINE)) {
+  dim3 grid(splits, static_cast<unsigned>(a.n_units));
+  decode_generic_kernel<<<grid, kNW * 32, shm, s>>>(c, a.group, a.q, a.q_dtype, a.sm_scale * kLog2e, a.scores,
+                                                    a.scores_ld, ep, tps);
+  if (splits > 1 && a.out != nullptr && !(a.flags & PQB_DECODE_NO_COMBINE))
     combine_kernel<<<static_cast<unsigned>(a.n_units), 256, 0, s>>>(ep.part_ml, ep.part_o, splits, a.group, c.d,
                                                                     a.out, a.out_dtype);
-  }
   return PQB_OK;
 }
 

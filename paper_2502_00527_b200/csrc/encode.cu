@@ -403,7 +403,7 @@ __global__ void store_values_kernel(const void* __restrict__ vals, int src_dtype
     const int64_t ta = off + t;
     const int64_t page = ta / st.page_tokens;
     uint8_t* p = page_base(st, unit, page) + st.value_off +
-                 ((ta - page * st.page_tokens) * d + e) * vbytes;
+                 value_offset(ta - page * st.page_tokens, e, d, st.value_dtype);
     if (vbytes == 4) *reinterpret_cast<float*>(p) = v;
     else *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
   }
@@ -472,10 +472,10 @@ __global__ void __launch_bounds__(256) append_kernel(pqb_cache c, const void* __
         v = val_dtype == PQB_F32 ? load1<PQB_F32>(vals, ko)
                                  : (val_dtype == PQB_BF16 ? load1<PQB_BF16>(vals, ko) : load1<PQB_F16>(vals, ko));
       const int64_t page = T / c.store.page_tokens;
-      uint8_t* p = page_base(c.store, unit, page) + c.store.value_off;
-      const int64_t idx = (T - page * c.store.page_tokens) * d + e;
-      if (c.store.value_dtype == PQB_F32) reinterpret_cast<float*>(p)[idx] = v;
-      else reinterpret_cast<__nv_bfloat16*>(p)[idx] = __float2bfloat16_rn(v);
+      uint8_t* p = page_base(c.store, unit, page) + c.store.value_off +
+                   value_offset(T - page * c.store.page_tokens, e, d, c.store.value_dtype);
+      if (c.store.value_dtype == PQB_F32) *reinterpret_cast<float*>(p) = v;
+      else *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
     }
   }
   if (bad) atomicOr(flags, PQB_FLAG_NONFINITE);
