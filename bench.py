@@ -3,14 +3,24 @@
 Headline workload (BASELINE.json configs[1]): Llama-3.1-8B decode attention,
 all 32 layers, batch 16, 32K context, 32 query / 8 KV heads, d=128, m=4/n=4
 polar keys + bf16 values.  One step = one decode step over all 32 layers (per
-layer one fused LUT-attention launch over its 128 (sequence, kv-head) units,
-captured in a CUDA graph).  value = sequences advanced per second.
+layer one fused LUT-attention launch over its 128 (sequence, kv-head) units
+plus the split merge, captured in a CUDA graph).  value = sequences advanced
+per second (tokens/s), whole job.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--shard batch|heads] [--no-extras]
 
-Multi-GPU: one process per GPU (torchrun), each rank owns its own 16
-sequences (batch sharding: every unit is independent, no data-path
-collective) -> "scaling": "weak", value = total over ranks, time = max over ranks.
+Multi-GPU (torchrun, one process per GPU):
+  --shard batch (default)  each rank owns its own 16 sequences: units are
+                           independent, no data-path collective -> "weak".
+  --shard heads            configs[2]/[3] style: the fixed global batch is split
+                           by KV head; every layer all-gathers the head outputs
+                           over NCCL -> "strong".
+Time = max over ranks of the device-timed region.
+
+Extras (rank 0, 1 GPU, after the headline): configs[0] (small, latency),
+configs[2] at P=1 (128K ctx, m3n2), configs[3] per-GPU slice (70B head shape,
+one KV head of 8), configs[4] encoder slab.
 """
 
 from __future__ import annotations
@@ -19,7 +29,6 @@ import argparse
 import json
 import math
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -39,6 +48,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--shard", choices=["batch", "heads"], default="batch")
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--ctx", type=int, default=32768)
@@ -48,9 +58,9 @@ def parse():
     ap.add_argument("--n", type=int, default=4)
     ap.add_argument("--page-tokens", type=int, default=128)
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--no-encode", action="store_true", help="skip the config-5 encoder sub-benchmark")
+    ap.add_argument("--no-extras", action="store_true", help="skip configs 1/3/4/5 side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no timing claims)")
     return ap.parse_args()
 
@@ -67,47 +77,64 @@ def peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled with NVML every 20 ms while active."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = {  # nvmlClocksEventReason bits
+        0x8: "hw_slowdown",
+        0x40: "hw_thermal_slowdown",
+        0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap",
+        0x80: "hw_power_brake_slowdown",
+    }
 
-    def __init__(self, index: int):
-        self.index = index
-        self.rows: list[list[str]] = []
+    def __init__(self, torch_device):
+        self.samples: list[tuple[float, int]] = []
+        self.max_mhz = None
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._handle = None
+        try:
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(torch_device)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self._handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            self._nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._handle, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._handle = None
 
     def _run(self):
+        nv = self._nv
         while not self._stop.is_set():
             try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
-                    capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                clk = nv.nvmlDeviceGetClockInfo(self._handle, nv.NVML_CLOCK_SM)
+                reasons = nv.nvmlDeviceGetCurrentClocksEventReasons(self._handle)
+                self.samples.append((float(clk), int(reasons)))
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.02)
 
     def __enter__(self):
-        self._t.start()
+        if self._handle is not None:
+            self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
-        self._t.join(timeout=10)
+        if self._t.is_alive():
+            self._t.join(timeout=5)
 
     def summary(self) -> dict:
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        bits = 0
+        for _, r in self.samples:
+            bits |= r
+        return {"sm_mhz": float(np.median([c for c, _ in self.samples])), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(n for b, n in self.REASONS.items() if bits & b), "samples": len(self.samples)}
 
 
 def unit_bytes(T: int, G: int, d: int, m: int, n: int) -> int:
@@ -173,119 +200,164 @@ def cpu_baseline(T, d, m, n, G, units_per_step, batch, seconds: float) -> dict:
 # ------------------------------------------------------------------- ours
 
 
-def run_ours(a, rank: int, world: int, dist) -> dict | None:
-    import torch
+class DecodeWorkload:
+    """A multi-layer decode cache on one GPU plus its per-step launch sequence.
 
-    import paper_2502_00527_b200 as pq
-    from paper_2502_00527_b200 import _lib
+    layers x (batch x kv_heads) units, each with T tokens; one step runs every
+    layer's fused decode (optionally followed by the head-output gather)."""
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
-    torch.cuda.set_device(dev)
-    L, B, Hq, Hkv, T, d = a.layers, a.batch, a.hq, a.hkv, a.ctx, 128
-    G = Hq // Hkv
-    upl = B * Hkv  # units per layer
-    U = L * upl
-    cfg = pq.QuantConfig(a.m, a.n)
-    cache = pq.PolarKVCache(cfg, U, d, 0, capacity=T, page_tokens=a.page_tokens, value_dtype=torch.bfloat16,
-                            device=dev)
-    syn = pq.SyntheticConfig(T, d, outlier_channels=frozenset({0, 1}))
-    for layer in range(L):  # fill layer by layer (keeps the bf16 staging at 2 GB)
-        seed = (rank * 1000 + layer) * 7919 + 1
-        keys = pq.synthetic_keys_device(syn, upl, dtype=torch.bfloat16, device=dev, seed=seed)
-        vals = pq.normal_device((upl, T, d), seed + 1, dtype=torch.bfloat16, device=dev)
-        cache.prefill(keys, vals, unit_start=layer * upl, check=(layer == 0))
-        del keys, vals
-    q_all = pq.normal_device((L, upl, G, d), 424242 + rank, dtype=torch.bfloat16, device=dev)
-    out_all = torch.empty((L, upl, G, d), dtype=torch.bfloat16, device=dev)
-    views = [cache.view(layer * upl, (layer + 1) * upl) for layer in range(L)]
-    stream = torch.cuda.Stream(device=dev)
+    def __init__(self, dev, *, layers, batch, hq, hkv, T, m, n, page_tokens, seed, plan=None, group=None):
+        import torch
 
-    def step():
-        for layer in range(L):
-            views[layer].decode(q_all[layer], out=out_all[layer], max_tokens=T)
+        import paper_2502_00527_b200 as pq
 
-    def attn_only():
-        for layer in range(L):
-            views[layer].decode(q_all[layer], out=out_all[layer], max_tokens=T, flags=_lib.PQB_DECODE_NO_COMBINE)
+        self.dev, self.torch, self.pq = dev, torch, pq
+        self.L, self.T, self.m, self.n = layers, T, m, n
+        self.G = hq // hkv
+        self.plan, self.group = plan, group
+        self.upl = plan.units_per_layer if plan is not None else batch * hkv
+        self.batch, self.hq = batch, hq
+        cfg = pq.QuantConfig(m, n)
+        self.cache = pq.PolarKVCache(cfg, layers * self.upl, 128, 0, capacity=T, page_tokens=page_tokens,
+                                     value_dtype=torch.bfloat16, device=dev)
+        syn = pq.SyntheticConfig(T, 128, outlier_channels=frozenset({0, 1}))
+        chunk = max(1, min(self.upl, (1 << 31) // (T * 128 * 2)))  # <= 2 GB bf16 staging per tensor
+        for layer in range(layers):
+            for u0 in range(0, self.upl, chunk):
+                k = min(chunk, self.upl - u0)
+                s = (seed * 1000 + layer) * 7919 + u0 + 1
+                keys = pq.synthetic_keys_device(syn, k, dtype=torch.bfloat16, device=dev, seed=s)
+                vals = pq.normal_device((k, T, 128), s + 1, dtype=torch.bfloat16, device=dev)
+                self.cache.prefill(keys, vals, unit_start=layer * self.upl + u0, check=(layer == 0 and u0 == 0))
+                del keys, vals
+        self.q = pq.normal_device((layers, self.upl, self.G, 128), 424242 + seed, dtype=torch.bfloat16, device=dev)
+        self.out = torch.empty((layers, self.upl, self.G, 128), dtype=torch.bfloat16, device=dev)
+        self.views = [self.cache.view(i * self.upl, (i + 1) * self.upl) for i in range(layers)]
+        self.gathered = None
+        if plan is not None:
+            self.gathered = torch.empty((layers, batch, hq, 128), dtype=torch.bfloat16, device=dev)
+        self.stream = torch.cuda.Stream(device=dev)
 
-    with torch.cuda.stream(stream):
-        step()
-        attn_only()
-    torch.cuda.synchronize(dev)
-    splits = _lib.load().pqb_decode_splits(upl, T)
-    launches_per_step = L * (2 if splits > 1 else 1)
-    graph = None
-    if not a.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            step()
-        graph_attn = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph_attn, stream=stream):
-            attn_only()
-    run = graph.replay if graph else step
-    run_attn = graph_attn.replay if graph else attn_only
+    def step(self, flags: int = 0):
+        for i in range(self.L):
+            self.views[i].decode(self.q[i], out=self.out[i], max_tokens=self.T, flags=flags)
+            if self.gathered is not None:
+                from paper_2502_00527_b200.sharding import gather_head_outputs
 
-    if a.profile:
-        with torch.cuda.stream(stream):
-            for _ in range(max(1, a.steps)):
-                step()
-        torch.cuda.synchronize(dev)
-        return None
+                self.gathered[i].copy_(gather_head_outputs(self.out[i], self.plan, self.group))
 
-    def timed(fn, steps: int, warmup: int) -> float:
-        with torch.cuda.stream(stream):
+    def launches_per_step(self) -> int:
+        return 2 * self.L  # fused decode + split merge per layer
+
+    def bytes_per_launch(self) -> int:
+        return self.upl * unit_bytes(self.T, self.G, 128, self.m, self.n)
+
+    def capture(self, fn):
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
+            fn()
+        torch.cuda.synchronize(self.dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            fn()
+        return g.replay
+
+    def timed(self, fn, steps: int, warmup: int, dist=None) -> float:
+        torch = self.torch
+        with torch.cuda.stream(self.stream):
             for _ in range(warmup):
                 fn()
-        torch.cuda.synchronize(dev)
+        torch.cuda.synchronize(self.dev)
         if dist:
             dist.barrier()
-        torch.cuda.synchronize(dev)
+        torch.cuda.synchronize(self.dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
+        with torch.cuda.stream(self.stream):
+            e0.record(self.stream)
             for _ in range(steps):
                 fn()
-            e1.record(stream)
-        torch.cuda.synchronize(dev)
+            e1.record(self.stream)
+        torch.cuda.synchronize(self.dev)
         ms = e0.elapsed_time(e1) / steps
         if dist:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            t = torch.tensor([ms], device=self.dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
 
-    with ClockSampler(dev.index) as clk:
-        ms_step = timed(run, a.steps, a.warmup)
-    ms_attn_layer = timed(run_attn, max(3, a.steps // 2), 2) / L
+    def free(self):
+        del self.cache, self.q, self.out, self.views
+        self.torch.cuda.empty_cache()
+
+
+def measure_workload(w: DecodeWorkload, steps: int, warmup: int, graph: bool = True) -> dict:
+    """Step time (graph) + attention-kernel-only time per launch + roofline."""
+    from paper_2502_00527_b200 import _lib
+
+    run = w.capture(w.step) if graph else w.step
+    run_attn = w.capture(lambda: w.step(_lib.PQB_DECODE_NO_COMBINE)) if graph else (
+        lambda: w.step(_lib.PQB_DECODE_NO_COMBINE))
+    ms = w.timed(run, steps, warmup)
+    ms_attn = w.timed(run_attn, max(3, steps // 2), 2) / w.L
+    pk = peaks()
+    algo = w.bytes_per_launch()
+    return {"ms_per_step": ms, "tokens_per_s": w.batch / (ms * 1e-3), "avg_launch_ms": ms_attn,
+            "achieved_gbs": algo / (ms_attn * 1e-3) / 1e9, "frac": algo / (ms_attn * 1e-3) / 1e9 / pk["hbm_gbs"],
+            "step_frac": w.L * algo / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
+
+
+def run_ours(a, rank: int, world: int, dist) -> dict | None:
+    import torch
+
+    from paper_2502_00527_b200 import sharding
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    G = a.hq // a.hkv
+    plan = None
+    batch = a.batch
+    if a.shard == "heads" and world > 1:
+        shape = sharding.DecodeShape(a.layers, a.batch, a.hq, a.hkv)
+        plan = sharding.head_shard(shape, world, rank)
+    w = DecodeWorkload(dev, layers=a.layers, batch=batch, hq=a.hq, hkv=a.hkv, T=a.ctx, m=a.m, n=a.n,
+                       page_tokens=a.page_tokens, seed=rank, plan=plan)
+    if a.profile:
+        with torch.cuda.stream(w.stream):
+            for _ in range(max(1, a.steps)):
+                w.step()
+        torch.cuda.synchronize(dev)
+        return None
+    from paper_2502_00527_b200 import _lib
+
+    run = w.step if a.no_graph else w.capture(w.step)
+    with ClockSampler(dev) as clk:
+        ms_step = w.timed(run, a.steps, a.warmup, dist)
+    run_attn = (lambda: w.step(_lib.PQB_DECODE_NO_COMBINE))
+    run_attn = run_attn if a.no_graph else w.capture(run_attn)
+    ms_attn_layer = w.timed(run_attn, max(3, a.steps // 2), 2, dist) / a.layers
 
     # ---- e2e through the public API with host buffers (pinned), per step:
-    #      H2D of every layer's queries, 32 decode_attention calls, D2H of outputs.
-    q_host = q_all.cpu().pin_memory()
-    o_host = torch.empty(out_all.shape, dtype=out_all.dtype).pin_memory()
-    q_dev = torch.empty_like(q_all)
+    #      H2D of every layer's queries, per-layer decode calls, D2H of outputs.
+    q_host = w.q.cpu().pin_memory()
+    o_host = torch.empty(w.out.shape, dtype=w.out.dtype).pin_memory()
+    q_dev = torch.empty_like(w.q)
 
-    def e2e_step_api():
+    def e2e_step():
         q_dev.copy_(q_host, non_blocking=True)
-        for layer in range(L):
-            views[layer].decode(q_dev[layer], out=out_all[layer], max_tokens=T)
-        o_host.copy_(out_all, non_blocking=True)
+        for i in range(a.layers):
+            w.views[i].decode(q_dev[i], out=w.out[i], max_tokens=a.ctx)
+        o_host.copy_(w.out, non_blocking=True)
 
-    ms_e2e = timed(e2e_step_api, max(3, a.steps // 2), 2)
-
-    # ---- config-5 style encoder sub-benchmark (bulk prefill, bf16 keys)
-    enc = None
-    if not a.no_encode:
-        enc = encode_bench(dev, rank, a)
-
-    algo = upl * unit_bytes(T, G, d, a.m, a.n)  # per layer launch
+    ms_e2e = w.timed(e2e_step, max(3, a.steps // 2), 2, dist)
+    algo = w.bytes_per_launch()
     pk = peaks()
     achieved = algo / (ms_attn_layer * 1e-3) / 1e9
-    step_bytes = L * algo
-    return {
+    global_batch = a.batch * world if a.shard == "batch" else a.batch
+    res = {
         "ms_per_step": ms_step,
-        "value": B * world / (ms_step * 1e-3),
+        "value": global_batch / (ms_step * 1e-3),
         "e2e_ms": ms_e2e,
-        "e2e_value": B * world / (ms_e2e * 1e-3),
+        "e2e_value": global_batch / (ms_e2e * 1e-3),
         "h2d": q_host.numel() * q_host.element_size(),
         "d2h": o_host.numel() * o_host.element_size(),
         "roofline": {
@@ -295,17 +367,50 @@ def run_ours(a, rank: int, world: int, dist) -> dict | None:
             "unit": "GB/s",
             "frac": achieved / pk["hbm_gbs"],
             "peak_source": pk["source"],
-            "kernel": f"decode_fast_kernel<G={G},M={a.m},N={a.n}> (split partials, no combine)",
+            "kernel": f"decode_fast_kernel<G={G},M={a.m},N={a.n}> (persistent, split partials; merge excluded)",
             "algorithmic_bytes_per_launch": algo,
             "avg_launch_ms": ms_attn_layer,
-            "step_frac": step_bytes / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"],
+            "step_frac": a.layers * algo / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"],
             "traffic": ncu_traffic(),
         },
         "clocks": clk.summary(),
-        "gpu_launches": a.steps * launches_per_step,
-        "splits": splits,
-        "encode": enc,
+        "gpu_launches": a.steps * w.launches_per_step(),
+        "global_batch": global_batch,
     }
+    w.free()
+    del w
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not a.no_extras:
+        res["extras"] = run_extras(dev, a)
+    return res
+
+
+def run_extras(dev, a) -> dict:
+    """Side measurements of the other BASELINE configs on one GPU."""
+    import torch
+
+    out = {}
+    specs = {
+        "configs[0]_L1_B1_4K_m4n4": dict(layers=1, batch=1, hq=32, hkv=8, T=4096, m=4, n=4),
+        "configs[2]_P1_L32_B8_128K_m3n2": dict(layers=32, batch=8, hq=32, hkv=8, T=131072, m=3, n=2),
+        "configs[3]_per_gpu_L80_B32_32K_G8_1kvhead": dict(layers=80, batch=32, hq=8, hkv=1, T=32768, m=4, n=4),
+    }
+    for name, s in specs.items():
+        try:
+            w = DecodeWorkload(dev, page_tokens=a.page_tokens, seed=7, **s)
+            r = measure_workload(w, steps=max(3, a.steps // 2), warmup=2)
+            r["bytes_per_step"] = w.L * w.bytes_per_launch()
+            w.free()
+            del w
+            torch.cuda.empty_cache()
+            out[name] = r
+        except Exception as exc:  # report, never hide the headline
+            out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+    try:
+        out["configs[4]_encode"] = encode_bench(dev, a)
+    except Exception as exc:
+        out["configs[4]_encode"] = {"error": f"{type(exc).__name__}: {exc}"}
+    return out
 
 
 def ncu_traffic():
@@ -318,46 +423,50 @@ def ncu_traffic():
     return None
 
 
-def encode_bench(dev, rank: int, a) -> dict:
-    """Config 5 sample on one GPU: 32 layers x 8 kv heads x T tokens of bf16
-    keys through K1 (scales) + K2 (encode/pack), timed end to end on device."""
+def encode_bench(dev, a) -> dict:
+    """configs[4] slab on one GPU: 32 layers x 8 kv heads = 256 units x T bf16
+    tokens through K1 (scales) + K2 (encode/pack), device-timed, for every
+    (m, n) the config names."""
     import torch
 
     import paper_2502_00527_b200 as pq
-
-    T = 131072  # tokens per unit in the timed slab (config 5 is 1M; per-unit work is linear in T)
-    U = 256
-    d = 128
-    syn = pq.SyntheticConfig(T, d, outlier_channels=frozenset({0, 1}))
-    keys = pq.synthetic_keys_device(syn, U, dtype=torch.bfloat16, device=dev, seed=99 + rank)
-    cfg = pq.QuantConfig(4, 4)
-    cache = pq.PolarKVCache(cfg, U, d, 0, capacity=T, page_tokens=256, value_dtype=torch.bfloat16, device=dev)
-    flags = torch.zeros(1, dtype=torch.int32, device=dev)
-    ws = torch.empty(U * 64, dtype=torch.int64, device=dev)
     from paper_2502_00527_b200.codec import encode_device, radius_scales_device
 
-    def once():
-        radius_scales_device(keys, cfg, flags, ws, out=cache.scales16)
-        encode_device(keys, cache.scales16, cfg, cache.store_ref(), clamp_counts=cache.clamp_counts, flags=flags)
-
-    for _ in range(2):
-        once()
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    reps = 5
-    e0.record()
-    for _ in range(reps):
-        once()
-    e1.record()
-    torch.cuda.synchronize(dev)
-    ms = e0.elapsed_time(e1) / reps
-    algo = U * (2 * T * d * 2 + T * (d // 2) * 8 // 8 + (d // 2) * 2)
+    T, U, d = 131072, 256, 128  # config 5 is 1M tokens/unit; cost is linear in T
+    syn = pq.SyntheticConfig(T, d, outlier_channels=frozenset({0, 1}))
+    keys = pq.synthetic_keys_device(syn, U, dtype=torch.bfloat16, device=dev, seed=99)
+    flags = torch.zeros(1, dtype=torch.int32, device=dev)
+    ws = torch.empty(U * 64, dtype=torch.int64, device=dev)
     pk = peaks()
-    del keys, cache
+    res = {"workload": f"{U} units x {T} tokens bf16 keys (configs[4] slab; scales + encode + pack)"}
+    for m, n in [(4, 4), (3, 2), (2, 4)]:
+        cfg = pq.QuantConfig(m, n)
+        cache = pq.PolarKVCache(cfg, U, d, 0, capacity=T, page_tokens=256, value_dtype=torch.bfloat16, device=dev)
+
+        def once():
+            radius_scales_device(keys, cfg, flags, ws, out=cache.scales16)
+            encode_device(keys, cache.scales16, cfg, cache.store_ref(), clamp_counts=cache.clamp_counts,
+                          flags=flags)
+
+        for _ in range(2):
+            once()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 5
+        e0.record()
+        for _ in range(reps):
+            once()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        ms = e0.elapsed_time(e1) / reps
+        algo = U * (2 * T * d * 2 + T * (d // 2) * (m + n) // 8 + (d // 2) * 2)
+        res[f"m{m}n{n}"] = {"ms": ms, "token_heads_per_s": U * T / (ms * 1e-3),
+                            "achieved_gbs": algo / (ms * 1e-3) / 1e9,
+                            "frac": algo / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
+        del cache
+    del keys
     torch.cuda.empty_cache()
-    return {"workload": f"encode {U} units x {T} tokens bf16 (config-5 slab), m4n4", "ms": ms,
-            "token_heads_per_s": U * T / (ms * 1e-3), "achieved_gbs": algo / (ms * 1e-3) / 1e9,
-            "frac": algo / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    return res
 
 
 # ------------------------------------------------------------------- main
@@ -378,18 +487,23 @@ def main() -> None:
     G = a.hq // a.hkv
     upl = a.batch * a.hkv
     units_per_step = a.layers * upl
+    heads = a.shard == "heads" and world > 1
     config = {"workload": "configs[1]: Llama-3.1-8B heads (32 Q / 8 KV, d=128), 32 layers, batch 16/GPU, 32K ctx, "
                           "m=4 angle / n=4 radius bits, bf16 V; one step = one decode step over all layers",
-              "layers": a.layers, "batch_per_gpu": a.batch, "global_batch": a.batch * world, "ctx": a.ctx,
+              "layers": a.layers, "batch_per_gpu": a.batch if not heads else a.batch, "ctx": a.ctx,
+              "global_batch": a.batch * world if not heads else a.batch,
               "q_heads": a.hq, "kv_heads": a.hkv, "head_dim": 128, "angle_bits": a.m, "radius_bits": a.n,
-              "page_tokens": a.page_tokens, "parallelism": f"batch-sharded x{world} (no collective)",
+              "page_tokens": a.page_tokens,
+              "parallelism": (f"kv-head sharded x{world} + per-layer NCCL all-gather" if heads
+                              else f"batch-sharded x{world} (no collective)"),
               "l2": "inputs (43 GB cache per GPU) >> 126 MB L2; no flush needed"}
 
     if a.impl == "reference":
         if rank == 0:
             steps = []
             for i in range(a.warmup + a.steps):
-                cb = cpu_baseline(a.ctx, 128, a.m, a.n, G, units_per_step, a.batch, seconds=max(2.0, a.cpu_seconds / 4))
+                cb = cpu_baseline(a.ctx, 128, a.m, a.n, G, units_per_step, a.batch,
+                                  seconds=max(1.0, a.cpu_seconds / 5))
                 if i >= a.warmup:
                     steps.append(cb)
             v = float(np.mean([s["value"] for s in steps]))
@@ -401,6 +515,7 @@ def main() -> None:
                     "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
             print(json.dumps(line), flush=True)
         if dist:
+            dist.barrier()
             dist.destroy_process_group()
         return
 
@@ -422,7 +537,7 @@ def main() -> None:
             "warmup": a.warmup,
             "ms_per_step": res["ms_per_step"],
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong" if heads else "weak",
             "vs_baseline": None,
             "dtype": "f32",
             "data": "synthetic (on-device Philox: lognormal radii, uniform angles, 2 outlier channels)",
@@ -433,8 +548,7 @@ def main() -> None:
                     "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"]},
             "clocks": res["clocks"],
             "gpu_launches": res["gpu_launches"],
-            "decode_splits": res["splits"],
-            "encode": res["encode"],
+            "extras": res.get("extras"),
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -233,7 +233,7 @@ class PolarKVCache:
                 v = v.unsqueeze(0)
             if tuple(v.shape) != tuple(k.shape):
                 raise ValueError(f"values shape {tuple(v.shape)} != {tuple(k.shape)}")
-        self.ensure_capacity(T + 1)
+        self.ensure_capacity(T)
         sub = self.sub_struct(u0, u1)
         sref = ctypes.byref(sub)
         n = u1 - u0

@@ -119,8 +119,10 @@ int pqb_encode(const void* keys, int key_dtype, int64_t n_units, int64_t tokens,
   if (rc) return rc;
   if (n_units == 0 || tokens == 0) return PQB_OK;
   const int half = d / 2;
+  // vector kernel: whole 32-bit words per token (half % 32 == 0) and one block
+  // iteration (256 / (half/8) tokens) crossing at most one page boundary
   const bool vec = vec_loads_ok(keys, key_dtype, d, unit_stride, tok_stride) && half % 32 == 0 &&
-                   reinterpret_cast<uintptr_t>(scales) % 16 == 0;
+                   2048 / half <= store->page_tokens && reinterpret_cast<uintptr_t>(scales) % 16 == 0;
   EncodeArgs a{keys, key_dtype, n_units, tokens, d, unit_stride, tok_stride, layout, angle_bits, radius_bits,
                scales, store, tok_offset, tok_offset_const, clamp_counts, flags, vec};
   launch_encode(a, reinterpret_cast<cudaStream_t>(stream));

@@ -111,6 +111,29 @@ struct CodeLanes {
   }
 };
 
+// A token's 8B code bytes from the stage (lane-strided rows of 8B bytes).  For
+// B = 4 (32-byte rows) the two 16-byte halves are read in lane-dependent order
+// so a quarter-warp's LDS.128 touches 8 distinct bank groups (no 2-way conflict).
+template <int B>
+PQB_DEV void load_token_codes(const uint8_t* row, int lane, uint32_t* w) {
+  if constexpr (B == 4) {
+    const uint32_t sw = (lane >> 2) & 1u;
+    const uint4 v0 = *reinterpret_cast<const uint4*>(row + (sw << 4));
+    const uint4 v1 = *reinterpret_cast<const uint4*>(row + ((sw ^ 1u) << 4));
+    const uint4 lo = sw ? v1 : v0, hi = sw ? v0 : v1;
+    w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
+    w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
+  } else {
+    const uint2* p = reinterpret_cast<const uint2*>(row);
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const uint2 v = p[i];
+      w[2 * i] = v.x;
+      w[2 * i + 1] = v.y;
+    }
+  }
+}
+
 // ---- tensor-core helpers
 
 PQB_DEV void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -297,12 +320,8 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       for (int g = 0; g < G; ++g) acc[g] = 0.0f;
       if (tok < Tq) {
         uint32_t wa[2 * M + 1], wr[2 * N + 1];
-        const uint2* pa = reinterpret_cast<const uint2*>(st + lane * 8 * M);
-        const uint2* pr = reinterpret_cast<const uint2*>(st + Cfg::kABytes + lane * 8 * N);
-#pragma unroll
-        for (int i = 0; i < M; ++i) { const uint2 v = pa[i]; wa[2 * i] = v.x; wa[2 * i + 1] = v.y; }
-#pragma unroll
-        for (int i = 0; i < N; ++i) { const uint2 v = pr[i]; wr[2 * i] = v.x; wr[2 * i + 1] = v.y; }
+        load_token_codes<M>(st + lane * 8 * M, lane, wa);
+        load_token_codes<N>(st + Cfg::kABytes + lane * 8 * N, lane, wr);
         wa[2 * M] = 0u;
         wr[2 * N] = 0u;
         CodeLanes<M, Cfg::kS> ca;

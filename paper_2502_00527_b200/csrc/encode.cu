@@ -34,13 +34,21 @@ PQB_DEV bool finite2(float x, float y) { return fabsf(x) <= 3.40282347e38f && fa
 
 // ------------------------------------------------------------------ K1
 
+// The exact per-channel maximum of d2 = fl64(x^2 + y^2) needs double precision
+// only for candidates: f = fl32(x*x + fl32(y*y)) is within 2^-23 (relative) of
+// d2, so any element whose d2 could be the maximum has f >= (running max of f)
+// * (1 - 2^-20).  Only those take the double path; for random data that is a
+// vanishing fraction after the first few tokens.  A token row's eight channels
+// share one branch.  NaN/Inf inputs always become candidates (their f bits
+// compare above any finite threshold) and propagate through the integer max
+// of the double bits into the scale, where finalize flags them.
 template <int DT, int LAYOUT>
 __global__ void __launch_bounds__(256) radius_max_v8_kernel(const void* __restrict__ keys, int64_t T,
                                                             int half, int64_t unit_stride,
                                                             int64_t tok_stride, int64_t chunk,
                                                             unsigned long long* __restrict__ maxsq,
                                                             int32_t* __restrict__ flags) {
-  __shared__ double s_red[8][256];  // [channel-in-group][thread]
+  __shared__ unsigned long long s_red[8][256];  // [channel-in-group][thread]
   const int unit = blockIdx.y;
   const int tpr = half >> 3;  // threads per token row
   const int rows = 256 / tpr;
@@ -48,10 +56,15 @@ __global__ void __launch_bounds__(256) radius_max_v8_kernel(const void* __restri
   const int64_t t_begin = static_cast<int64_t>(blockIdx.x) * chunk;
   const int64_t t_end = min(T, t_begin + chunk);
   const int64_t ubase = static_cast<int64_t>(unit) * unit_stride;
-  double mx[8];
+  unsigned long long dmax[8];  // exact max of d2 (double bits; non-negative -> integer order)
+  uint32_t thr[8];             // candidate threshold on f bits
+  float fmax_[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) mx[i] = 0.0;
-  bool bad = false;
+  for (int i = 0; i < 8; ++i) {
+    dmax[i] = 0ull;
+    thr[i] = 0u;
+    fmax_[i] = 0.0f;
+  }
   for (int64_t t = t_begin + row; t < t_end; t += rows) {
     float x[8], y[8];
     const int64_t rb = ubase + t * tok_stride;
@@ -68,23 +81,38 @@ __global__ void __launch_bounds__(256) radius_max_v8_kernel(const void* __restri
         x[4 + i] = v1[2 * i]; y[4 + i] = v1[2 * i + 1];
       }
     }
+    float f[8];
+    bool cand = false;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      bad |= !finite2(x[i], y[i]);
-      const double xd = x[i], yd = y[i];
-      mx[i] = fmax(mx[i], __fma_rn(xd, xd, __dmul_rn(yd, yd)));
+      f[i] = fmaf(x[i], x[i], y[i] * y[i]);
+      cand |= __float_as_uint(f[i]) >= thr[i];
+    }
+    if (cand) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (__float_as_uint(f[i]) >= thr[i]) {
+          const double xd = x[i], yd = y[i];
+          const unsigned long long db = dbits(__fma_rn(xd, xd, __dmul_rn(yd, yd)));
+          dmax[i] = db > dmax[i] ? db : dmax[i];
+          fmax_[i] = fmaxf(fmax_[i], f[i]);
+          thr[i] = __float_as_uint(fmax_[i] * (1.0f - 0x1p-20f));
+          if (!(f[i] <= 3.40282347e38f)) thr[i] = 0u;  // non-finite: keep everything a candidate
+        }
+      }
     }
   }
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flags, PQB_FLAG_NONFINITE);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) s_red[i][threadIdx.x] = mx[i];
+  for (int i = 0; i < 8; ++i) s_red[i][threadIdx.x] = dmax[i];
   __syncthreads();
-  // thread c < half reduces channel c over all rows
   for (int c = threadIdx.x; c < half; c += 256) {
     const int g = c >> 3, i = c & 7;
-    double m = 0.0;
-    for (int r = 0; r < rows; ++r) m = fmax(m, s_red[i][r * tpr + g]);
-    if (m > 0.0) atomicMax(maxsq + static_cast<int64_t>(unit) * half + c, dbits(m));
+    unsigned long long m = 0ull;
+    for (int r = 0; r < rows; ++r) {
+      const unsigned long long v = s_red[i][r * tpr + g];
+      m = v > m ? v : m;
+    }
+    if (m) atomicMax(maxsq + static_cast<int64_t>(unit) * half + c, m);
   }
 }
 
@@ -128,6 +156,7 @@ __global__ void scales_finalize_kernel(const unsigned long long* __restrict__ ma
   const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= count) return;
   const double d2 = __longlong_as_double(static_cast<long long>(maxsq[i]));
+  if (!(d2 <= 1.79769313486231570815e308)) atomicOr(flags, PQB_FLAG_NONFINITE);  // NaN/Inf keys
   const float top = __double2float_rn(__dsqrt_rn(d2));                 // radius.max(axis=0), fp32
   const float s = __fdiv_rn(top, static_cast<float>((1 << n_bits) - 1));  // fp32 / int
   const __half h = __float2half_rn(s);                                  // ChannelScales -> fp16
@@ -207,7 +236,16 @@ __global__ void __launch_bounds__(256) encode_v8_kernel(const void* __restrict__
   const int wpt_a = half * M / 32, wpt_r = half * n_bits / 32;  // 32-bit words per token
   const int cb_a = 8 * M, cb_r = 8 * n_bits;
   const int nch_a = chunks_per_word(M), nch_r = chunks_per_word(n_bits);
-  const int64_t page_tok = st.page_tokens;
+  // words this lane stores per pass: w = lane + 32*k; token / word-in-token are lane constants
+  const int tw_a0 = lane / wpt_a, wi_a0 = lane - tw_a0 * wpt_a;
+  const int tw_a1 = (lane + 32) / wpt_a, wi_a1 = lane + 32 - tw_a1 * wpt_a;
+  const int tw_r0 = lane / wpt_r, wi_r0 = lane - tw_r0 * wpt_r;
+  const int tw_r1 = (lane + 32) / wpt_r, wi_r1 = lane + 32 - tw_r1 * wpt_r;
+  // page position of the block-iteration's first token (rows <= page_tokens:
+  // one iteration crosses at most one page boundary)
+  const int P = st.page_tokens;
+  int64_t pg = (off + t_begin) / P;
+  int in_pg = static_cast<int>(off + t_begin - pg * P);
   uint32_t clamps = 0;
   bool bad = false;
 
@@ -234,16 +272,18 @@ __global__ void __launch_bounds__(256) encode_v8_kernel(const void* __restrict__
 #pragma unroll
       for (int i = 0; i < 8; ++i) x[i] = y[i] = 0.0f;
     }
+    uint32_t a[8], r[8];
+    encode8<M>(x, y, s32, inv, n_bits, valid, a, r, clamps, bad, s_tan, s_thr);
     unsigned long long ca = 0ull, cr = 0ull;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      bad |= !finite2(x[i], y[i]);
-      uint32_t a, r;
-      encode_pair<M>(x[i], y[i], s32[i], inv[i], n_bits, a, r, clamps, s_tan, s_thr);
-      ca |= static_cast<unsigned long long>(a) << (M * i);
-      cr |= static_cast<unsigned long long>(r) << (n_bits * i);
+      ca |= static_cast<unsigned long long>(a[i]) << (M * i);
+      cr |= static_cast<unsigned long long>(r[i]) << (n_bits * i);
     }
     if (!valid) ca = cr = 0ull;
+    // pages of this iteration (uniform): pg, and pg+1 if the rows cross into it
+    const uint8_t* pb0 = page_base(st, unit, pg);
+    const uint8_t* pb1 = (in_pg + rows > P && base + (P - in_pg) < t_end) ? page_base(st, unit, pg + 1) : pb0;
     // ---- assemble and store the warp's 8*M angle words and 8*n radius words
 #pragma unroll
     for (int pass = 0; pass < 2; ++pass) {
@@ -253,21 +293,29 @@ __global__ void __launch_bounds__(256) encode_v8_kernel(const void* __restrict__
       const int wpt = pass == 0 ? wpt_a : wpt_r;
       const int64_t region = pass == 0 ? st.angle_off : st.radius_off;
       const unsigned long long chunk_bits = pass == 0 ? ca : cr;
-      for (int w0 = 0; w0 < 8 * b; w0 += 32) {  // warp-uniform
-        const int w = w0 + lane;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (32 * k >= 8 * b) break;  // warp-uniform
+        const int w = 32 * k + lane;
         const uint32_t word = warp_word(chunk_bits, cb, nch, w);
-        if (w < 8 * b) {
-          const int tw = w / wpt;
-          const int64_t t_call = base + warp_row0 + tw;
-          if (t_call < t_end) {
-            const int64_t t_abs = off + t_call;
-            const int64_t page = t_abs / page_tok;
-            uint8_t* p = page_base(st, unit, page) + region +
-                         ((t_abs - page * page_tok) * wpt + (w - tw * wpt)) * 4;
-            *reinterpret_cast<uint32_t*>(p) = word;
+        const int tw = pass == 0 ? (k ? tw_a1 : tw_a0) : (k ? tw_r1 : tw_r0);
+        const int wi = pass == 0 ? (k ? wi_a1 : wi_a0) : (k ? wi_r1 : wi_r0);
+        if (w < 8 * b && base + warp_row0 + tw < t_end) {
+          int in_w = in_pg + warp_row0 + tw;
+          const uint8_t* pb = pb0;
+          if (in_w >= P) {
+            in_w -= P;
+            pb = pb1;
           }
+          *reinterpret_cast<uint32_t*>(const_cast<uint8_t*>(pb) + region + (static_cast<int64_t>(in_w) * wpt + wi) * 4) =
+              word;
         }
       }
+    }
+    in_pg += rows;
+    while (in_pg >= P) {
+      in_pg -= P;
+      ++pg;
     }
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(flags, PQB_FLAG_NONFINITE);
@@ -382,6 +430,38 @@ __global__ void __launch_bounds__(256) encode_generic_kernel(GenericSrc src, int
 }
 
 // ------------------------------------------------------------- values
+
+// d = 128 bf16 pages: one thread per (token, 16-byte chunk) -> one 128-bit
+// store at the chunk's swizzled slot (value_offset()).
+template <int DT>
+__global__ void store_values_v8_kernel(const void* __restrict__ vals, int64_t T, int64_t unit_stride,
+                                       int64_t tok_stride, pqb_store st, int64_t tok_offset_const) {
+  const int64_t unit = blockIdx.y;
+  const int64_t n = T * 16;
+  const int P = st.page_tokens;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i >> 4;
+    const int c = static_cast<int>(i & 15);
+    uint4 w = make_uint4(0u, 0u, 0u, 0u);
+    if (vals) {
+      float v[8];
+      load8<DT>(vals, unit * unit_stride + t * tok_stride + 8 * c, v);
+      uint32_t* wp = reinterpret_cast<uint32_t*>(&w);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const __nv_bfloat162 b = __floats2bfloat162_rn(v[2 * k], v[2 * k + 1]);
+        wp[k] = *reinterpret_cast<const uint32_t*>(&b);
+      }
+    }
+    const int64_t ta = tok_offset_const + t;
+    const int64_t page = ta / P;
+    const int64_t tp = ta - page * P;
+    uint8_t* dst = page_base(st, unit, page) + st.value_off + tp * 256 + ((c ^ static_cast<int>(tp & 7)) << 4);
+    *reinterpret_cast<uint4*>(dst) = w;
+  }
+}
+
 
 __global__ void store_values_kernel(const void* __restrict__ vals, int src_dtype, int64_t T, int d,
                                     int64_t unit_stride, int64_t tok_stride, pqb_store st,
@@ -601,6 +681,18 @@ int launch_encode(const EncodeArgs& a, cudaStream_t s) {
 int launch_store_values(const void* vals, int dtype, int64_t n_units, int64_t T, int d, int64_t us, int64_t ts,
                         const pqb_store& st, const int32_t* tok_offset, int64_t tok_offset_const, cudaStream_t s) {
   if (T == 0) return 0;
+  const int eb = dtype == PQB_F32 ? 4 : 2;
+  const bool vec = d == 128 && st.value_dtype == PQB_BF16 && tok_offset == nullptr && st.value_off % 16 == 0 &&
+                   st.page_bytes % 16 == 0 && (vals == nullptr || (reinterpret_cast<uintptr_t>(vals) % 16 == 0 &&
+                                                                   (us * eb) % 16 == 0 && (ts * eb) % 16 == 0));
+  if (vec) {
+    const int64_t n = T * 16;
+    dim3 grid(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096)), static_cast<unsigned>(n_units));
+    if (dtype == PQB_F32) store_values_v8_kernel<PQB_F32><<<grid, 256, 0, s>>>(vals, T, us, ts, st, tok_offset_const);
+    else if (dtype == PQB_F16) store_values_v8_kernel<PQB_F16><<<grid, 256, 0, s>>>(vals, T, us, ts, st, tok_offset_const);
+    else store_values_v8_kernel<PQB_BF16><<<grid, 256, 0, s>>>(vals, T, us, ts, st, tok_offset_const);
+    return 0;
+  }
   const int64_t n = T * d;
   dim3 grid(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 4096)), static_cast<unsigned>(n_units));
   store_values_kernel<<<grid, 256, 0, s>>>(vals, dtype, T, d, us, ts, st, tok_offset, tok_offset_const);

@@ -59,24 +59,30 @@ PQB_DEV float radius_raw_exact(float x, float y, float s) {
 
 // ------------------------------------------------------------- fast paths
 
+// |v| in [2^-100, 2^100] as one unsigned compare on the float bits (false for
+// 0, subnormals, huge values, Inf and NaN): the range where the fp32 edge tests
+// below are provably accurate.
+PQB_DEV bool in_safe_range(float v) {
+  return (__float_as_uint(v) & 0x7fffffffu) - 0x0D800000u <= (0x71800000u - 0x0D800000u);
+}
+
 // Angle code for angle_bits M; sets amb when the point is within DELTA of a bin
-// edge (or the input magnitude is outside the range where the fp32 edge test is
-// reliable) and the caller must use angle_code_exact.
+// edge (or outside the safe magnitude range) and the caller must use
+// angle_code_exact.  Edge constants fold into FFMA/FMUL immediates.
 template <int M>
 PQB_DEV uint32_t angle_code_fast(float x, float y, bool& amb, const float* smem_tan,
                                  const float* smem_thr) {
   const float ax = fabsf(x), ay = fabsf(y);
   const uint32_t sx = __float_as_uint(x) >> 31, sy = __float_as_uint(y) >> 31;
+  const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
+  amb = !in_safe_range(mx);
   if constexpr (M == 1) {
     // edges at phi = +-pi/2 (the y axis): code 1 iff x > 0
-    const float mx = fmaxf(ax, ay);
-    amb = !(ax > PQB_ANGLE_DELTA * (ax + ay)) || !(mx >= 0x1p-100f && mx <= 0x1p100f);
+    amb |= !(ax > PQB_ANGLE_DELTA * (ax + ay));
     return sx ? 0u : 1u;
   } else {
     constexpr int H = 1 << (M - 1);
     int k;  // bin index within the quadrant, 0 .. 2^(M-2)
-    const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-    amb = !(mx >= 0x1p-100f && mx <= 0x1p100f);
     if constexpr (M == 2) {
       const float dd = ay - ax;  // edge at pi/4; sign exact
       amb |= fabsf(dd) <= kQuadEdgeThr * (ax + ay);
@@ -88,9 +94,9 @@ PQB_DEV uint32_t angle_code_fast(float x, float y, bool& amb, const float* smem_
       if constexpr (NB <= 4) {
 #pragma unroll
         for (int i = 0; i < NB; ++i) {
-          const float di = fmaf(-mx, kEdgeTan[M][i], mn);
+          const float di = fmaf(-mx, edge_tan(M, i), mn);
           kk += di > 0.0f ? 1 : 0;
-          amb |= fabsf(di) <= kEdgeThr[M][i] * sum;
+          amb |= fabsf(di) <= edge_thr(M, i) * sum;
         }
       } else {
         // estimate psi = atan(mn/mx) to < step/4, then verify the two edges
@@ -124,51 +130,57 @@ PQB_DEV uint32_t angle_code_fast(float x, float y, bool& amb, const float* smem_
   }
 }
 
-// Fast radius raw code rint(r/s) for s > 0 (as a float; large values mean
-// "clamped").  Sets amb when the estimate is too close to a rounding edge or the
-// magnitude is outside the safe fp32 range.
+// Fast rint(r/s) (float; large values mean "clamped"), branch-free.  r is
+// estimated as r2 * rsqrt(r2) (relative error < 2^-21 with the fp32 rounding of
+// r2 and 1/s); amb when that estimate lies within 2^-18 (relative) of a
+// half-integer or r2 is outside the safe range (zero, subnormal, huge, NaN).
 PQB_DEV float radius_raw_fast(float x, float y, float inv_s, bool& amb) {
-  if (x == 0.0f && y == 0.0f) {
-    amb = false;
-    return 0.0f;
-  }
   const float r2 = fmaf(x, x, y * y);
-  amb = !(r2 >= 0x1p-100f && r2 <= 0x1p100f);
+  amb = !in_safe_range(r2);
   const float q = r2 * rsqrtf(r2) * inv_s;
-  if (q >= 1024.0f) return q;  // far above any top code (<= 255): certainly clamped
-  const float fl = floorf(q);
-  const float fr = q - fl;
-  amb |= fabsf(fr - 0.5f) <= 0x1p-18f * q;
-  return fr > 0.5f ? fl + 1.0f : fl;
+  const float rq = rintf(q);
+  amb |= fabsf(q - rq) >= fmaf(-0x1p-18f, q, 0.5f);
+  return rq;
 }
 
-// Full per-sub-vector encode (quantize_subvectors semantics) with the fast path
-// and exact fallback.  s32 is the fp16 scale widened to f32; inv_s = 1/s32.
+// Eight sub-vectors (one thread's channel group) with one divergent slow path:
+// fast codes for all eight, then the exact pipeline only for the flagged ones.
+// Returns codes in a[], r[]; counts clamps; s32 == 0 channels give (0, 0).
 template <int M>
-PQB_DEV void encode_pair(float x, float y, float s32, float inv_s, int n_bits, uint32_t& acode,
-                         uint32_t& rcode, uint32_t& clamped, const float* smem_tan,
-                         const float* smem_thr) {
-  if (s32 == 0.0f) {  // zero-scale channel: both codes 0 (polar_codec.py:298-301)
-    acode = 0u;
-    rcode = 0u;
-    return;
-  }
+PQB_DEV void encode8(const float (&x)[8], const float (&y)[8], const float (&s32)[8], const float (&inv)[8],
+                     int n_bits, bool valid, uint32_t (&a)[8], uint32_t (&r)[8], uint32_t& clamped,
+                     bool& bad, const float* smem_tan, const float* smem_thr) {
   const float top = static_cast<float>((1 << n_bits) - 1);
-  bool ramb;
-  float raw = radius_raw_fast(x, y, inv_s, ramb);
-  if (ramb) raw = radius_raw_exact(x, y, s32);
-  if (raw > top) {
-    clamped += 1u;
-    raw = top;
+  float raw[8];
+  uint32_t amb_mask = 0u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    bool ra, aa;
+    raw[i] = radius_raw_fast(x[i], y[i], inv[i], ra);
+    a[i] = angle_code_fast<M>(x[i], y[i], aa, smem_tan, smem_thr);
+    amb_mask |= static_cast<uint32_t>(ra | aa) << i;
   }
-  rcode = static_cast<uint32_t>(raw);
-  if (rcode == 0u) {  // canonical: origin's angle code (polar_codec.py:297)
-    acode = 1u << (M - 1);
-    return;
+  if (!valid) amb_mask = 0u;
+  if (amb_mask) {  // ~1e-5 of sub-vectors: exact double-precision pipeline
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if ((amb_mask >> i) & 1u) {
+        bad |= !(fabsf(x[i]) <= 3.40282347e38f && fabsf(y[i]) <= 3.40282347e38f);
+        raw[i] = s32[i] > 0.0f ? radius_raw_exact(x[i], y[i], s32[i]) : 0.0f;
+        a[i] = angle_code_exact(x[i], y[i], M);
+      }
+    }
   }
-  bool aamb;
-  acode = angle_code_fast<M>(x, y, aamb, smem_tan, smem_thr);
-  if (aamb) acode = angle_code_exact(x, y, M);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool over = raw[i] > top;
+    clamped += (over && valid && s32[i] > 0.0f) ? 1u : 0u;
+    uint32_t rc = static_cast<uint32_t>(fminf(raw[i], top));
+    uint32_t ac = rc == 0u ? (1u << (M - 1)) : a[i];  // canonical: origin's angle (polar_codec.py:297)
+    if (s32[i] == 0.0f) rc = ac = 0u;                  // zero-scale channel (polar_codec.py:298-301)
+    a[i] = ac;
+    r[i] = rc;
+  }
 }
 
 // Runtime-m variant: exact pipeline only (used by the generic / append paths).
