@@ -111,7 +111,6 @@ class PolarKVCache:
         self._filled = np.zeros(U, dtype=bool)
         self._all_view: UnitView | None = None
         self.prefilled = False
-        self._ws: torch.Tensor | None = None
         self.max_pages = 0
         self._alloc(max(int(capacity), 1))
 
@@ -307,12 +306,6 @@ class PolarKVCache:
 
     # ------------------------------------------------------------ decode
 
-    def workspace(self, n_units: int, group: int, max_tokens: int) -> torch.Tensor:
-        need = _lib.load().pqb_decode_workspace_bytes(n_units, group, max_tokens, self.dim)
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
-        return self._ws
-
     def _all(self) -> "UnitView":
         if self._all_view is None or self._all_view.struct.store.pool != ptr(self.pool):
             self._all_view = UnitView(self, 0, self.n_units)
@@ -397,6 +390,15 @@ class UnitView:
         self.n_units = u1 - u0
         self.struct = cache.sub_struct(u0, u1)
         self.ref = ctypes.byref(self.struct)
+        self._ws: torch.Tensor | None = None
+
+    def workspace(self, group: int, max_tokens: int) -> torch.Tensor:
+        """Per-view decode workspace.  Zero-filled once: its leading counter
+        region (split-merge bookkeeping) is left zeroed by every call."""
+        need = _lib.load().pqb_decode_workspace_bytes(self.n_units, group, max_tokens, self.cache.dim)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.cache.device)
+        return self._ws
 
     @property
     def max_tokens(self) -> int:
@@ -422,7 +424,7 @@ class UnitView:
             raise ValueError("cannot attend over an empty cache")
         if out is None:
             out = torch.empty((self.n_units, G, c.dim), dtype=out_dtype, device=c.device)
-        ws = c.workspace(self.n_units, G, T_max)
+        ws = self.workspace(G, T_max)
         scale = (1.0 / math.sqrt(c.dim)) if sm_scale is None else float(sm_scale)
         _lib.call(
             "pqb_decode_attn_ex", self.ref, self.n_units, G, ptr(q), dtype_code(q), scale, T_max, ptr(out),

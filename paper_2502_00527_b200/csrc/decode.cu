@@ -26,7 +26,10 @@
 //     from the tile with ldmatrix.trans (the page stores value rows XOR-swizzled,
 //     value_offset(), so the 8 rows of a fragment hit 8 bank groups); P is split
 //     into bf16 hi + lo (p - hi) so the product keeps ~2^-17 relative accuracy.
-//   Segment partials (m, l, o) are LSE-merged by combine_split_kernel.
+//   A CTA that covers a whole unit writes its output directly; otherwise it
+//   writes a segment partial (m, l, o) and the last CTA to finish the unit
+//   (atomic counter in the workspace) LSE-merges the partials -- one launch per
+//   decode call.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -157,7 +160,9 @@ struct EpiArgs {
   int out_dtype;
   float* part_ml;  // [n_units][slots][G][2]
   float* part_o;   // [n_units][slots][G][d]
+  int* counters;   // [n_units] finished-segment counts (zero between calls)
   int slots;       // partial slots per unit
+  bool merge;      // fast kernel: last CTA of a unit merges (else leave partials)
 };
 
 PQB_DEV void store_out(void* out, int dt, int64_t idx, float v) {
@@ -174,6 +179,26 @@ struct WorkSplit {
 };
 
 PQB_DEV int64_t first_cta(const WorkSplit& w, int64_t unit) { return (unit * w.tiles_max) / w.per_cta; }
+PQB_DEV int64_t last_cta(const WorkSplit& w, int64_t unit) { return ((unit + 1) * w.tiles_max - 1) / w.per_cta; }
+
+// LSE merge of a unit's segment partials: out = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M)
+PQB_DEV void merge_slots(const EpiArgs& ep, int64_t unit, int nseg, int G, int tid, int nthreads) {
+  for (int i = tid; i < G * 128; i += nthreads) {
+    const int g = i >> 7, e = i & 127;
+    float mx = -INFINITY;
+    for (int s = 0; s < nseg; ++s) mx = fmaxf(mx, __ldcg(ep.part_ml + 2 * ((unit * ep.slots + s) * G + g)));
+    float L = 0.0f, O = 0.0f;
+    for (int s = 0; s < nseg; ++s) {
+      const int64_t sl = (unit * ep.slots + s) * G + g;
+      const float ms = __ldcg(ep.part_ml + 2 * sl);
+      if (ms == -INFINITY) continue;
+      const float sc = exp2f(ms - mx);
+      L = fmaf(__ldcg(ep.part_ml + 2 * sl + 1), sc, L);
+      O = fmaf(__ldcg(ep.part_o + sl * 128 + e), sc, O);
+    }
+    store_out(ep.out, ep.out_dtype, (unit * G + g) * 128 + e, O / L);
+  }
+}
 
 // ------------------------------------------------------------------ fast kernel
 
@@ -476,7 +501,10 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       }
     }
     __syncthreads();
-    const int64_t slot = (unit * ep.slots + (blockIdx.x - first_cta(ws, unit))) * G;
+    const int64_t c_first = first_cta(ws, unit);
+    const int nseg = static_cast<int>(last_cta(ws, unit) - c_first + 1);
+    const bool direct = nseg == 1;  // this CTA covers the whole unit: write the output
+    const int64_t slot = (unit * ep.slots + (blockIdx.x - c_first)) * G;
     for (int i = tid; i < G * 128; i += blockDim.x) {
       const int g = i >> 7, e = i & 127;
       float mx = -INFINITY;
@@ -492,37 +520,37 @@ __global__ void __launch_bounds__(kNW * 32, 1)
           O = fmaf(rw[4 + e], sc, O);
         }
       }
-      ep.part_o[(slot + g) * 128 + e] = O;
-      if (e == 0) {
-        ep.part_ml[2 * (slot + g)] = mx;
-        ep.part_ml[2 * (slot + g) + 1] = L;
+      if (direct && ep.merge) {
+        store_out(ep.out, ep.out_dtype, (unit * G + g) * 128 + e, O / L);
+      } else {
+        ep.part_o[(slot + g) * 128 + e] = O;
+        if (e == 0) {
+          ep.part_ml[2 * (slot + g)] = mx;
+          ep.part_ml[2 * (slot + g) + 1] = L;
+        }
       }
+    }
+    if (direct || !ep.merge) continue;
+    // ---- the last CTA to finish a unit merges its segments (no extra launch)
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last;
+    if (tid == 0) s_last = atomicAdd(ep.counters + unit, 1) == nseg - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      merge_slots(ep, unit, nseg, G, tid, blockDim.x);
+      if (tid == 0) ep.counters[unit] = 0;  // leave the workspace zeroed for the next call
     }
   }
 }
 
-// LSE merge of the per-(unit, CTA) partials of decode_fast_kernel.
-__global__ void combine_split_kernel(const float* __restrict__ part_ml, const float* __restrict__ part_o,
-                                     WorkSplit ws, int slots, int G, void* out, int out_dtype) {
+// Stand-alone merge of decode_fast_kernel partials (used when the in-kernel
+// merge is disabled, e.g. kernel-only timing followed by an explicit merge).
+__global__ void combine_split_kernel(EpiArgs ep, WorkSplit ws, int G) {
   const int64_t unit = blockIdx.x;
-  const int64_t c0 = first_cta(ws, unit);
-  const int64_t c1 = ((unit + 1) * ws.tiles_max - 1) / ws.per_cta;
-  const int n = static_cast<int>(c1 - c0 + 1);
-  for (int i = threadIdx.x; i < G * 128; i += blockDim.x) {
-    const int g = i >> 7, e = i & 127;
-    float mx = -INFINITY;
-    for (int s = 0; s < n; ++s) mx = fmaxf(mx, part_ml[2 * ((unit * slots + s) * G + g)]);
-    float L = 0.0f, O = 0.0f;
-    for (int s = 0; s < n; ++s) {
-      const int64_t sl = (unit * slots + s) * G + g;
-      const float ms = part_ml[2 * sl];
-      if (ms == -INFINITY) continue;
-      const float sc = exp2f(ms - mx);
-      L = fmaf(part_ml[2 * sl + 1], sc, L);
-      O = fmaf(part_o[sl * 128 + e], sc, O);
-    }
-    store_out(out, out_dtype, (unit * G + g) * 128 + e, O / L);
-  }
+  const int nseg = static_cast<int>(last_cta(ws, unit) - first_cta(ws, unit) + 1);
+  merge_slots(ep, unit, nseg, G, threadIdx.x, blockDim.x);
 }
 
 // ------------------------------------------------------------------ generic kernel
@@ -729,9 +757,18 @@ static int fast_slots(int64_t n_units, int max_tokens) {
 
 int decode_splits(int64_t n_units, int max_tokens) { return choose_splits(n_units, max_tokens); }
 
-size_t decode_workspace_bytes(int64_t n_units, int group, int max_tokens, int d) {
+// workspace: [counters: n_units ints, 256-B rounded][partials: n_units * slots * G * (2 + d) floats]
+// The counter region sits at a fixed offset for a given n_units, is zero before
+// the first call and is left zeroed by every fused call.
+static size_t counter_bytes(int64_t n_units) { return (static_cast<size_t>(n_units) * sizeof(int) + 255) / 256 * 256; }
+
+static size_t partial_bytes(int64_t n_units, int group, int max_tokens, int d) {
   const int s = std::max(max_splits(max_tokens), fast_slots(n_units, max_tokens));
-  return static_cast<size_t>(n_units) * s * group * (2 + d) * sizeof(float) + 256;
+  return static_cast<size_t>(n_units) * s * group * (2 + d) * sizeof(float);
+}
+
+size_t decode_workspace_bytes(int64_t n_units, int group, int max_tokens, int d) {
+  return counter_bytes(n_units) + partial_bytes(n_units, group, max_tokens, d) + 256;
 }
 
 template <int G, int M, int N, bool EXACT>
@@ -753,10 +790,12 @@ static int launch_fast(const DecodeArgs& a, cudaStream_t s) {
   ep.out = a.out;
   ep.out_dtype = a.out_dtype;
   ep.slots = fast_slots(a.n_units, a.max_tokens);
-  ep.part_ml = static_cast<float*>(a.workspace);
+  ep.counters = static_cast<int*>(a.workspace);
+  ep.part_ml = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + counter_bytes(a.n_units));
   ep.part_o = ep.part_ml + a.n_units * ep.slots * G * 2;
+  ep.merge = !(a.flags & PQB_DECODE_NO_COMBINE);
   if (a.out != nullptr) {
-    const size_t need = static_cast<size_t>(a.n_units) * ep.slots * G * (2 + 128) * sizeof(float);
+    const size_t need = decode_workspace_bytes(a.n_units, a.group, a.max_tokens, 128);
     if (a.workspace == nullptr || a.workspace_bytes < need) {
       set_error("decode workspace too small: need %zu bytes, got %zu", need, a.workspace_bytes);
       return PQB_EINVAL;
@@ -764,9 +803,6 @@ static int launch_fast(const DecodeArgs& a, cudaStream_t s) {
   }
   decode_fast_kernel<G, M, N, EXACT><<<grid, kNW * 32, Cfg::kSmem, s>>>(
       *a.cache, a.q, a.q_dtype, a.sm_scale * kLog2e, a.scores, a.scores_ld, ep, ws);
-  if (a.out != nullptr && !(a.flags & PQB_DECODE_NO_COMBINE))
-    combine_split_kernel<<<static_cast<unsigned>(a.n_units), 128, 0, s>>>(ep.part_ml, ep.part_o, ws, ep.slots, G,
-                                                                           a.out, a.out_dtype);
   return PQB_OK;
 }
 
@@ -815,10 +851,14 @@ int launch_decode(const DecodeArgs& a, cudaStream_t s) {
   ep.out = a.out;
   ep.out_dtype = a.out_dtype;
   ep.slots = splits;
-  ep.part_ml = static_cast<float*>(a.workspace);
+  // partials after the (untouched) counter region of the fast path
+  ep.part_ml = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + counter_bytes(a.n_units));
   ep.part_o = ep.part_ml + a.n_units * splits * a.group * 2;
+  ep.counters = nullptr;
+  ep.merge = false;
   if (splits > 1 && a.out != nullptr) {
-    const size_t need = static_cast<size_t>(a.n_units) * splits * a.group * (2 + c.d) * sizeof(float);
+    const size_t need = counter_bytes(a.n_units) +
+                        static_cast<size_t>(a.n_units) * splits * a.group * (2 + c.d) * sizeof(float);
     if (a.workspace == nullptr || a.workspace_bytes < need) {
       set_error("decode workspace too small: need %zu bytes, got %zu", need, a.workspace_bytes);
       return PQB_EINVAL;

@@ -57,16 +57,13 @@ __global__ void __launch_bounds__(256) radius_max_v8_kernel(const void* __restri
   const int64_t t_end = min(T, t_begin + chunk);
   const int64_t ubase = static_cast<int64_t>(unit) * unit_stride;
   unsigned long long dmax[8];  // exact max of d2 (double bits; non-negative -> integer order)
-  uint32_t thr[8];             // candidate threshold on f bits
-  float fmax_[8];
+  uint32_t thr[8];             // candidate threshold on f bits (f >= 0: integer order; NaN sorts high)
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     dmax[i] = 0ull;
     thr[i] = 0u;
-    fmax_[i] = 0.0f;
   }
-  for (int64_t t = t_begin + row; t < t_end; t += rows) {
-    float x[8], y[8];
+  auto load_row = [&](int64_t t, float (&x)[8], float (&y)[8]) {
     const int64_t rb = ubase + t * tok_stride;
     if constexpr (LAYOUT == PQB_HALF_SPLIT) {
       load8<DT>(keys, rb + 8 * cg, x);
@@ -81,6 +78,8 @@ __global__ void __launch_bounds__(256) radius_max_v8_kernel(const void* __restri
         x[4 + i] = v1[2 * i]; y[4 + i] = v1[2 * i + 1];
       }
     }
+  };
+  auto consider = [&](const float (&x)[8], const float (&y)[8]) {
     float f[8];
     bool cand = false;
 #pragma unroll
@@ -95,12 +94,29 @@ __global__ void __launch_bounds__(256) radius_max_v8_kernel(const void* __restri
           const double xd = x[i], yd = y[i];
           const unsigned long long db = dbits(__fma_rn(xd, xd, __dmul_rn(yd, yd)));
           dmax[i] = db > dmax[i] ? db : dmax[i];
-          fmax_[i] = fmaxf(fmax_[i], f[i]);
-          thr[i] = __float_as_uint(fmax_[i] * (1.0f - 0x1p-20f));
-          if (!(f[i] <= 3.40282347e38f)) thr[i] = 0u;  // non-finite: keep everything a candidate
+          const uint32_t nt = __float_as_uint(f[i] * (1.0f - 0x1p-20f));
+          thr[i] = f[i] <= 3.40282347e38f ? (nt > thr[i] ? nt : thr[i]) : 0u;  // non-finite: all candidates
         }
       }
     }
+  };
+  // four token rows per iteration: all loads issued before any use
+  int64_t t = t_begin + row;
+  for (; t + 3 * rows < t_end; t += 4 * rows) {
+    float x0[8], y0[8], x1[8], y1[8], x2[8], y2[8], x3[8], y3[8];
+    load_row(t, x0, y0);
+    load_row(t + rows, x1, y1);
+    load_row(t + 2 * rows, x2, y2);
+    load_row(t + 3 * rows, x3, y3);
+    consider(x0, y0);
+    consider(x1, y1);
+    consider(x2, y2);
+    consider(x3, y3);
+  }
+  for (; t < t_end; t += rows) {
+    float x0[8], y0[8];
+    load_row(t, x0, y0);
+    consider(x0, y0);
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) s_red[i][threadIdx.x] = dmax[i];
@@ -233,6 +249,9 @@ __global__ void __launch_bounds__(256) encode_v8_kernel(const void* __restrict__
 #pragma unroll
     for (int i = 0; i < 8; ++i) inv[i] = s32[i] > 0.0f ? __frcp_rn(s32[i]) : 0.0f;
   }
+  uint32_t nz_mask = 0u;  // channels with a non-zero scale
+#pragma unroll
+  for (int i = 0; i < 8; ++i) nz_mask |= static_cast<uint32_t>(s32[i] > 0.0f) << i;
   const int wpt_a = half * M / 32, wpt_r = half * n_bits / 32;  // 32-bit words per token
   const int cb_a = 8 * M, cb_r = 8 * n_bits;
   const int nch_a = chunks_per_word(M), nch_r = chunks_per_word(n_bits);
@@ -272,15 +291,8 @@ __global__ void __launch_bounds__(256) encode_v8_kernel(const void* __restrict__
 #pragma unroll
       for (int i = 0; i < 8; ++i) x[i] = y[i] = 0.0f;
     }
-    uint32_t a[8], r[8];
-    encode8<M>(x, y, s32, inv, n_bits, valid, a, r, clamps, bad, s_tan, s_thr);
-    unsigned long long ca = 0ull, cr = 0ull;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      ca |= static_cast<unsigned long long>(a[i]) << (M * i);
-      cr |= static_cast<unsigned long long>(r[i]) << (n_bits * i);
-    }
-    if (!valid) ca = cr = 0ull;
+    unsigned long long ca, cr;
+    encode8<M>(x, y, s32, inv, n_bits, valid ? nz_mask : 0u, ca, cr, clamps, bad, s_tan, s_thr);
     // pages of this iteration (uniform): pg, and pg+1 if the rows cross into it
     const uint8_t* pb0 = page_base(st, unit, pg);
     const uint8_t* pb1 = (in_pg + rows > P && base + (P - in_pg) < t_end) ? page_base(st, unit, pg + 1) : pb0;

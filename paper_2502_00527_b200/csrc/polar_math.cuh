@@ -134,10 +134,16 @@ PQB_DEV uint32_t angle_code_fast(float x, float y, bool& amb, const float* smem_
 // estimated as r2 * rsqrt(r2) (relative error < 2^-21 with the fp32 rounding of
 // r2 and 1/s); amb when that estimate lies within 2^-18 (relative) of a
 // half-integer or r2 is outside the safe range (zero, subnormal, huge, NaN).
+PQB_DEV float rsqrt_approx(float v) {  // MUFU.RSQ; v is in the safe range when used
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 PQB_DEV float radius_raw_fast(float x, float y, float inv_s, bool& amb) {
   const float r2 = fmaf(x, x, y * y);
   amb = !in_safe_range(r2);
-  const float q = r2 * rsqrtf(r2) * inv_s;
+  const float q = r2 * rsqrt_approx(r2) * inv_s;
   const float rq = rintf(q);
   amb |= fabsf(q - rq) >= fmaf(-0x1p-18f, q, 0.5f);
   return rq;
@@ -145,13 +151,16 @@ PQB_DEV float radius_raw_fast(float x, float y, float inv_s, bool& amb) {
 
 // Eight sub-vectors (one thread's channel group) with one divergent slow path:
 // fast codes for all eight, then the exact pipeline only for the flagged ones.
-// Returns codes in a[], r[]; counts clamps; s32 == 0 channels give (0, 0).
+// Returns the packed angle / radius chunks (code i at bits [b*i, b*(i+1))).
+// live: bit i set when sub-vector i is a valid token with a non-zero scale;
+// other positions produce (0, 0) (zero-scale rule, polar_codec.py:298-301).
 template <int M>
 PQB_DEV void encode8(const float (&x)[8], const float (&y)[8], const float (&s32)[8], const float (&inv)[8],
-                     int n_bits, bool valid, uint32_t (&a)[8], uint32_t (&r)[8], uint32_t& clamped,
-                     bool& bad, const float* smem_tan, const float* smem_thr) {
+                     int n_bits, uint32_t live, unsigned long long& ca, unsigned long long& cr,
+                     uint32_t& clamped, bool& bad, const float* smem_tan, const float* smem_thr) {
   const float top = static_cast<float>((1 << n_bits) - 1);
   float raw[8];
+  uint32_t a[8];
   uint32_t amb_mask = 0u;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -160,27 +169,40 @@ PQB_DEV void encode8(const float (&x)[8], const float (&y)[8], const float (&s32
     a[i] = angle_code_fast<M>(x[i], y[i], aa, smem_tan, smem_thr);
     amb_mask |= static_cast<uint32_t>(ra | aa) << i;
   }
-  if (!valid) amb_mask = 0u;
+  amb_mask &= live;
   if (amb_mask) {  // ~1e-5 of sub-vectors: exact double-precision pipeline
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       if ((amb_mask >> i) & 1u) {
         bad |= !(fabsf(x[i]) <= 3.40282347e38f && fabsf(y[i]) <= 3.40282347e38f);
-        raw[i] = s32[i] > 0.0f ? radius_raw_exact(x[i], y[i], s32[i]) : 0.0f;
+        raw[i] = radius_raw_exact(x[i], y[i], s32[i]);
         a[i] = angle_code_exact(x[i], y[i], M);
       }
     }
   }
+  uint32_t over = 0u;
+  ca = 0ull;
+  cr = 0ull;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    const bool over = raw[i] > top;
-    clamped += (over && valid && s32[i] > 0.0f) ? 1u : 0u;
-    uint32_t rc = static_cast<uint32_t>(fminf(raw[i], top));
-    uint32_t ac = rc == 0u ? (1u << (M - 1)) : a[i];  // canonical: origin's angle (polar_codec.py:297)
-    if (s32[i] == 0.0f) rc = ac = 0u;                  // zero-scale channel (polar_codec.py:298-301)
-    a[i] = ac;
-    r[i] = rc;
+    over |= static_cast<uint32_t>(raw[i] > top) << i;
+    const uint32_t rc = static_cast<uint32_t>(fminf(raw[i], top));
+    const uint32_t ac = rc == 0u ? (1u << (M - 1)) : a[i];  // canonical: origin's angle (polar_codec.py:297)
+    ca |= static_cast<unsigned long long>(ac) << (M * i);
+    cr |= static_cast<unsigned long long>(rc) << (n_bits * i);
   }
+  clamped += __popc(over & live);
+  // zero-scale channels and invalid tokens: both codes 0
+  unsigned long long ka = 0ull, kr = 0ull;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    if ((live >> i) & 1u) {
+      ka |= ((1ull << M) - 1ull) << (M * i);
+      kr |= ((1ull << n_bits) - 1ull) << (n_bits * i);
+    }
+  }
+  ca &= ka;
+  cr &= kr;
 }
 
 // Runtime-m variant: exact pipeline only (used by the generic / append paths).
