@@ -57,6 +57,31 @@ PQB_DEV void load8(const void* base, int64_t elem_off, float (&out)[8]) {
   }
 }
 
+// 8 consecutive elements from shared memory (16-byte aligned), widened to f32.
+template <int DT>
+PQB_DEV void load8s(const void* base, int elem_off, float (&out)[8]) {
+  if constexpr (DT == PQB_F32) {
+    const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(base) + elem_off);
+    const float4 a = p[0], b = p[1];
+    out[0] = a.x; out[1] = a.y; out[2] = a.z; out[3] = a.w;
+    out[4] = b.x; out[5] = b.y; out[6] = b.z; out[7] = b.w;
+  } else {
+    const uint4 w = *reinterpret_cast<const uint4*>(static_cast<const typename DType<DT>::T*>(base) + elem_off);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if constexpr (DT == PQB_BF16) {
+        out[2 * i] = __uint_as_float(ws[i] << 16);
+        out[2 * i + 1] = __uint_as_float(ws[i] & 0xffff0000u);
+      } else {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&ws[i]));
+        out[2 * i] = f.x;
+        out[2 * i + 1] = f.y;
+      }
+    }
+  }
+}
+
 template <int DT>
 PQB_DEV float load1(const void* base, int64_t elem_off) {
   return to_f32(static_cast<const typename DType<DT>::T*>(base)[elem_off]);

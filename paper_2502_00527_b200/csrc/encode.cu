@@ -132,6 +132,117 @@ __global__ void __launch_bounds__(256) radius_max_v8_kernel(const void* __restri
   }
 }
 
+// Same reduction for dense rows (tok_stride == d) fed by the TMA bulk-copy
+// engine: a 4-stage ring of 16 KB row blocks per CTA keeps ~64 KB per CTA in
+// flight independent of register pressure; threads read their 8-channel
+// slices from shared memory.
+constexpr int kRmaxStages = 4;
+constexpr int kRmaxStageBytes = 16384;
+
+template <int DT, int LAYOUT>
+__global__ void __launch_bounds__(256) radius_max_tma_kernel(const void* __restrict__ keys, int64_t T, int half,
+                                                             int64_t unit_stride, int64_t chunk,
+                                                             unsigned long long* __restrict__ maxsq) {
+  extern __shared__ __align__(128) uint8_t rsm[];
+  __shared__ uint64_t bars[kRmaxStages];
+  constexpr int EB = DType<DT>::kBytes;
+  const int unit = blockIdx.y;
+  const int d = 2 * half;
+  const int row_bytes = d * EB;
+  const int rows_per_stage = kRmaxStageBytes / row_bytes;
+  const int tpr = half >> 3;
+  const int rows = 256 / tpr;
+  const int cg = threadIdx.x % tpr, row = threadIdx.x / tpr;
+  const int64_t t_begin = static_cast<int64_t>(blockIdx.x) * chunk;
+  const int64_t t_end = min(T, t_begin + chunk);
+  const int n_stages = static_cast<int>((t_end - t_begin + rows_per_stage - 1) / rows_per_stage);
+  const uint8_t* src = static_cast<const uint8_t*>(keys) + (static_cast<int64_t>(unit) * unit_stride + t_begin * d) * EB;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRmaxStages; ++s) mbar_init(bars + s, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int k) {
+    const int64_t r0 = static_cast<int64_t>(k) * rows_per_stage;
+    const int64_t left = (t_end - t_begin) - r0;
+    const int nr = left < rows_per_stage ? static_cast<int>(left) : rows_per_stage;
+    const int slot = k % kRmaxStages;
+    mbar_arrive_expect_tx(bars + slot, nr * row_bytes);
+    bulk_g2s(rsm + slot * kRmaxStageBytes, src + r0 * row_bytes, nr * row_bytes, bars + slot);
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < kRmaxStages && k < n_stages; ++k) issue(k);
+  unsigned long long dmax[8];
+  uint32_t thr[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    dmax[i] = 0ull;
+    thr[i] = 0u;
+  }
+  for (int k = 0; k < n_stages; ++k) {
+    const int slot = k % kRmaxStages;
+    mbar_wait(bars + slot, (k / kRmaxStages) & 1);
+    const int64_t left = (t_end - t_begin) - static_cast<int64_t>(k) * rows_per_stage;
+    const int nr = left < rows_per_stage ? static_cast<int>(left) : rows_per_stage;
+    const uint8_t* st = rsm + slot * kRmaxStageBytes;
+    for (int r = row; r < nr; r += rows) {
+      float x[8], y[8];
+      const void* rp = st + r * row_bytes;
+      if constexpr (LAYOUT == PQB_HALF_SPLIT) {
+        load8s<DT>(rp, 8 * cg, x);
+        load8s<DT>(rp, half + 8 * cg, y);
+      } else {
+        float v0[8], v1[8];
+        load8s<DT>(rp, 16 * cg, v0);
+        load8s<DT>(rp, 16 * cg + 8, v1);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          x[i] = v0[2 * i]; y[i] = v0[2 * i + 1];
+          x[4 + i] = v1[2 * i]; y[4 + i] = v1[2 * i + 1];
+        }
+      }
+      float f[8];
+      bool cand = false;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        f[i] = fmaf(x[i], x[i], y[i] * y[i]);
+        cand |= __float_as_uint(f[i]) >= thr[i];
+      }
+      if (cand) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          if (__float_as_uint(f[i]) >= thr[i]) {
+            const double xd = x[i], yd = y[i];
+            const unsigned long long db = dbits(__fma_rn(xd, xd, __dmul_rn(yd, yd)));
+            dmax[i] = db > dmax[i] ? db : dmax[i];
+            const uint32_t nt = __float_as_uint(f[i] * (1.0f - 0x1p-20f));
+            thr[i] = f[i] <= 3.40282347e38f ? (nt > thr[i] ? nt : thr[i]) : 0u;
+          }
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with this slot
+    if (threadIdx.x == 0 && k + kRmaxStages < n_stages) {
+      fence_proxy_async_smem();
+      issue(k + kRmaxStages);
+    }
+  }
+  // block reduction of the per-thread maxima (reuse stage memory)
+  unsigned long long* red = reinterpret_cast<unsigned long long*>(rsm);  // [8][256]
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[i * 256 + threadIdx.x] = dmax[i];
+  __syncthreads();
+  for (int c = threadIdx.x; c < half; c += 256) {
+    const int g = c >> 3, i = c & 7;
+    unsigned long long m = 0ull;
+    for (int r = 0; r < rows; ++r) {
+      const unsigned long long v = red[i * 256 + r * tpr + g];
+      m = v > m ? v : m;
+    }
+    if (m) atomicMax(maxsq + static_cast<int64_t>(unit) * half + c, m);
+  }
+}
+
 // Any even d / layout / stride / alignment; one element pair per thread step.
 template <int DT>
 __global__ void __launch_bounds__(256) radius_max_generic_kernel(const void* __restrict__ keys, int64_t T,
@@ -590,12 +701,37 @@ static void launch_rmax_v8(const RadiusScalesArgs& a, int64_t chunk, dim3 grid, 
                                                         chunk, a.maxsq_ws, a.flags);
 }
 
+template <int DT, int LAYOUT>
+static void launch_rmax_tma(const RadiusScalesArgs& a, int64_t chunk, dim3 grid, size_t shm, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(radius_max_tma_kernel<DT, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(shm));
+    attr = true;
+  }
+  radius_max_tma_kernel<DT, LAYOUT><<<grid, 256, shm, s>>>(a.keys, a.tokens, a.d / 2, a.unit_stride, chunk,
+                                                           a.maxsq_ws);
+}
+
 int launch_radius_scales(const RadiusScalesArgs& a, cudaStream_t s) {
   const int half = a.d / 2;
   cudaMemsetAsync(a.maxsq_ws, 0, sizeof(unsigned long long) * a.n_units * half, s);
   const int64_t chunk = 4096;
   dim3 grid(static_cast<unsigned>((a.tokens + chunk - 1) / chunk), static_cast<unsigned>(a.n_units));
-  if (a.vector_ok) {
+  const int eb = a.key_dtype == PQB_F32 ? 4 : 2;
+  const bool dense = a.vector_ok && a.tok_stride == a.d && (static_cast<int64_t>(a.d) * eb) % 16 == 0 &&
+                     kRmaxStageBytes % (a.d * eb) == 0 && (a.unit_stride * eb) % 16 == 0;
+  if (dense) {
+    const size_t shm = kRmaxStages * kRmaxStageBytes;
+    switch (a.key_dtype * 2 + a.layout) {
+      case PQB_F32 * 2 + PQB_ADJACENT: launch_rmax_tma<PQB_F32, PQB_ADJACENT>(a, chunk, grid, shm, s); break;
+      case PQB_F32 * 2 + PQB_HALF_SPLIT: launch_rmax_tma<PQB_F32, PQB_HALF_SPLIT>(a, chunk, grid, shm, s); break;
+      case PQB_BF16 * 2 + PQB_ADJACENT: launch_rmax_tma<PQB_BF16, PQB_ADJACENT>(a, chunk, grid, shm, s); break;
+      case PQB_BF16 * 2 + PQB_HALF_SPLIT: launch_rmax_tma<PQB_BF16, PQB_HALF_SPLIT>(a, chunk, grid, shm, s); break;
+      case PQB_F16 * 2 + PQB_ADJACENT: launch_rmax_tma<PQB_F16, PQB_ADJACENT>(a, chunk, grid, shm, s); break;
+      default: launch_rmax_tma<PQB_F16, PQB_HALF_SPLIT>(a, chunk, grid, shm, s); break;
+    }
+  } else if (a.vector_ok) {
     switch (a.key_dtype * 2 + a.layout) {
       case PQB_F32 * 2 + PQB_ADJACENT: launch_rmax_v8<PQB_F32, PQB_ADJACENT>(a, chunk, grid, s); break;
       case PQB_F32 * 2 + PQB_HALF_SPLIT: launch_rmax_v8<PQB_F32, PQB_HALF_SPLIT>(a, chunk, grid, s); break;

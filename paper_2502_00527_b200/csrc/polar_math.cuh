@@ -65,6 +65,9 @@ PQB_DEV float radius_raw_exact(float x, float y, float s) {
 PQB_DEV bool in_safe_range(float v) {
   return (__float_as_uint(v) & 0x7fffffffu) - 0x0D800000u <= (0x71800000u - 0x0D800000u);
 }
+// Same for a value that is +0, positive or NaN (r2 = x*x + y*y): no abs mask
+// needed (a sign-bit NaN lands far above the range).
+PQB_DEV bool in_safe_range_nonneg(float v) { return __float_as_uint(v) - 0x0D800000u <= (0x71800000u - 0x0D800000u); }
 
 // Angle code for angle_bits M; sets amb when the point is within DELTA of a bin
 // edge (or outside the safe magnitude range) and the caller must use
@@ -75,7 +78,9 @@ PQB_DEV uint32_t angle_code_fast(float x, float y, bool& amb, const float* smem_
   const float ax = fabsf(x), ay = fabsf(y);
   const uint32_t sx = __float_as_uint(x) >> 31, sy = __float_as_uint(y) >> 31;
   const float mx = fmaxf(ax, ay), mn = fminf(ax, ay);
-  amb = !in_safe_range(mx);
+  // magnitude range: guaranteed by the caller's r2 check (r2 in [2^-100, 2^100]
+  // => mx in [2^-51, 2^50], where every edge product below is a normal float)
+  amb = false;
   if constexpr (M == 1) {
     // edges at phi = +-pi/2 (the y axis): code 1 iff x > 0
     amb |= !(ax > PQB_ANGLE_DELTA * (ax + ay));
@@ -142,7 +147,7 @@ PQB_DEV float rsqrt_approx(float v) {  // MUFU.RSQ; v is in the safe range when 
 
 PQB_DEV float radius_raw_fast(float x, float y, float inv_s, bool& amb) {
   const float r2 = fmaf(x, x, y * y);
-  amb = !in_safe_range(r2);
+  amb = !in_safe_range_nonneg(r2);
   const float q = r2 * rsqrt_approx(r2) * inv_s;
   const float rq = rintf(q);
   amb |= fabsf(q - rq) >= fmaf(-0x1p-18f, q, 0.5f);
@@ -161,19 +166,19 @@ PQB_DEV void encode8(const float (&x)[8], const float (&y)[8], const float (&s32
   const float top = static_cast<float>((1 << n_bits) - 1);
   float raw[8];
   uint32_t a[8];
-  uint32_t amb_mask = 0u;
+  bool any_amb = false;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     bool ra, aa;
     raw[i] = radius_raw_fast(x[i], y[i], inv[i], ra);
     a[i] = angle_code_fast<M>(x[i], y[i], aa, smem_tan, smem_thr);
-    amb_mask |= static_cast<uint32_t>(ra | aa) << i;
+    any_amb |= ra | aa;
   }
-  amb_mask &= live;
-  if (amb_mask) {  // ~1e-5 of sub-vectors: exact double-precision pipeline
+  if (any_amb && live) {  // ~1e-5 of sub-vectors: the exact double-precision pipeline for
+                          // this thread's eight (cheaper than tracking which one)
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      if ((amb_mask >> i) & 1u) {
+      if ((live >> i) & 1u) {
         bad |= !(fabsf(x[i]) <= 3.40282347e38f && fabsf(y[i]) <= 3.40282347e38f);
         raw[i] = radius_raw_exact(x[i], y[i], s32[i]);
         a[i] = angle_code_exact(x[i], y[i], M);

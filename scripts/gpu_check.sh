@@ -11,6 +11,9 @@ for f in tests/test_gpu_encode.py tests/test_gpu_decode.py tests/test_gpu_api.py
 done
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -5 gpurun_out/smoke.log
 if [ "${SKIP_BENCH:-0}" != "1" ]; then
-  timeout 900 python bench.py --steps 10 --warmup 3 --cpu-seconds 8 ${BENCH_ARGS:-} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
+  timeout 1200 python bench.py --steps 10 --warmup 3 --cpu-seconds 8 ${BENCH_ARGS:-} > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
   tail -5 gpurun_out/bench.err; cat gpurun_out/bench.json
+fi
+if [ "${NCU_ENCODE:-0}" = "1" ]; then
+  ncu --clock-control none --set full --import-source on -k regex:radius_max -s 2 -c 1 -o gpurun_out/rmax_latest -f python scripts/encode_probe.py > /dev/null 2>&1; echo "rmax ncu rc=$?"
 fi

@@ -222,3 +222,35 @@ def test_state_errors():
     with pytest.raises(ValueError):
         bad.prefill(np.full((4, 16), np.nan, np.float32))
     assert not bad.prefilled
+
+
+def test_views_and_workspace_reuse():
+    """Per-layer views (the benchmark's launch pattern) equal the full-cache
+    decode, and one view's workspace survives calls of different shapes
+    (the fused split merge leaves its counters zeroed)."""
+    L, upl, T = 3, 5, 3000
+    U = L * upl
+    keys = np.stack([po.synthetic_keys(T, 128, seed=900 + u) for u in range(U)])
+    rng = np.random.default_rng(5)
+    vals = torch.from_numpy(rng.standard_normal((U, T, 128)).astype(np.float32)).to(torch.bfloat16)
+    cache = pq.PolarKVCache(pq.QuantConfig(4, 4), U, 128, 0, capacity=T)
+    for layer in range(L):  # fill layer by layer through unit_start
+        sl = slice(layer * upl, (layer + 1) * upl)
+        cache.prefill(torch.from_numpy(keys[sl]).cuda(), vals[sl].cuda(), unit_start=layer * upl)
+    assert cache.prefilled
+    q4 = torch.from_numpy(rng.standard_normal((U, 4, 128)).astype(np.float32)).cuda()
+    full = cache.decode(q4).cpu().numpy()
+    view = cache.view(upl, 2 * upl)
+    for rep in range(3):
+        got = view.decode(q4[upl:2 * upl]).cpu().numpy()
+        np.testing.assert_allclose(got, full[upl:2 * upl], rtol=0, atol=1e-6)
+        q8 = torch.from_numpy(rng.standard_normal((upl, 8, 128)).astype(np.float32)).cuda()
+        o8 = view.decode(q8, max_tokens=T).cpu().numpy()
+        o8b = view.decode(q8, max_tokens=T, splits=7).cpu().numpy()  # different work split, same view
+        np.testing.assert_allclose(o8, o8b, rtol=0, atol=2e-6)
+        vb = vals.float().numpy().astype(np.float64)
+        for u in range(upl):
+            a, r = (t.cpu().numpy() for t in cache.code_arrays(upl + u))
+            s16 = cache.scales16[upl + u].cpu().numpy()
+            ref = po.softmax64(exact.lut_scores(q8[u, 3].cpu().numpy(), a, r, s16, 4, 4, 1), 1 / math.sqrt(128))
+            peak_close(o8[u, 3], ref @ vb[upl + u], OUT_RTOL_F32)
