@@ -36,12 +36,16 @@ constexpr float kTwoPiF = 6.28318548202514648438f;  // fl32(2 pi) == 2 * fl32(pi
 
 // ------------------------------------------------------------ exact paths
 
-PQB_DEV uint32_t angle_code_exact(float x, float y, int m) {
-  const float a = __double2float_rn(atan2(static_cast<double>(y), static_cast<double>(x)));
+// Steps 2-3 of the pipeline from the (correctly rounded) fp32 angle a.
+PQB_DEV uint32_t angle_code_from_phi(float a, int m) {
   float t = __fadd_rn(a, kPiF);
   if (t >= kTwoPiF) t = 0.0f;  // np.mod(t, fl32(2 pi)); t <= 2 pi_f32 by construction
   const float u = __fmul_rn(t, kAngleScale[m]);
   return static_cast<uint32_t>(__float2int_rn(u)) & ((1u << m) - 1u);
+}
+
+PQB_DEV uint32_t angle_code_exact(float x, float y, int m) {
+  return angle_code_from_phi(__double2float_rn(atan2(static_cast<double>(y), static_cast<double>(x))), m);
 }
 
 // fl32(sqrt(fl64(x^2 + y^2))): both squares are exact in double, one rounding
@@ -90,6 +94,12 @@ PQB_DEV uint32_t angle_code_fast(float x, float y, bool& amb, const float* smem_
     int k;  // bin index within the quadrant, 0 .. 2^(M-2)
     if constexpr (M == 2) {
       const float dd = ay - ax;  // edge at pi/4; sign exact
+      if (dd == 0.0f) {
+        // exactly on the diagonal (frequent for bf16 keys): atan2f is
+        // fl32(+-pi/4) or fl32(+-3pi/4), so finish the pipeline directly
+        // instead of sending the whole group down the double-precision path
+        return angle_code_from_phi(copysignf(sx ? 2.35619449615478515625f : 0.785398185253143310546875f, y), 2);
+      }
       amb |= fabsf(dd) <= kQuadEdgeThr * (ax + ay);
       k = dd > 0.0f ? 1 : 0;
     } else {

@@ -257,3 +257,22 @@ def test_edge_points_take_exact_path():
             ea, er, _ = exact.encode(keys, s.values, mm, n, layout.value)
             assert np.array_equal(codes.angle_codes(), ea), (layout, mm)
             assert np.array_equal(codes.radius_codes(), er)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_exact_diagonal_ties(m):
+    """|x| == |y| exactly (about 0.3% of bf16 pairs): the m = 2 bin edge; the
+    fast path resolves these without the double-precision fallback."""
+    rng = np.random.default_rng(11)
+    v = torch.from_numpy(rng.standard_normal((2048, 64)).astype(np.float32)).to(torch.bfloat16).float().numpy()
+    sx = rng.choice([-1.0, 1.0], size=v.shape).astype(np.float32)
+    sy = rng.choice([-1.0, 1.0], size=v.shape).astype(np.float32)
+    keys = np.concatenate([v * sx, v * sy], axis=1)  # HALF_SPLIT: x = dims[:64], y = dims[64:]
+    keys[::7, 5] = 0.0  # a few axis points too
+    cfg = pq.QuantConfig(m, 4)
+    cache = pq.PolarKVCache(cfg, 1, 128, 0, capacity=keys.shape[0] + 1)
+    cache.prefill(torch.from_numpy(keys).cuda().to(torch.bfloat16).unsqueeze(0))
+    s16 = exact.scales(keys, 4, 1)
+    ea, er, _ = exact.encode(keys, s16, m, 4, 1)
+    a, r = (t.cpu().numpy() for t in cache.code_arrays(0))
+    assert np.array_equal(a, ea) and np.array_equal(r, er)
