@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no timing claims)")
+    ap.add_argument("--variant", choices=["auto", "lut", "dq"], default="auto",
+                    help="scoring kernel of the fused decode (auto: the library's per-G choice)")
     return ap.parse_args()
 
 
@@ -237,10 +239,11 @@ class DecodeWorkload:
         if plan is not None:
             self.gathered = torch.empty((layers, batch, hq, 128), dtype=torch.bfloat16, device=dev)
         self.stream = torch.cuda.Stream(device=dev)
+        self.base_flags = 0  # PQB_DECODE_* bits added to every launch (kernel-variant probes)
 
     def step(self, flags: int = 0):
         for i in range(self.L):
-            self.views[i].decode(self.q[i], out=self.out[i], max_tokens=self.T, flags=flags)
+            self.views[i].decode(self.q[i], out=self.out[i], max_tokens=self.T, flags=flags | self.base_flags)
             if self.gathered is not None:
                 from paper_2502_00527_b200.sharding import gather_head_outputs
 
@@ -321,6 +324,9 @@ def run_ours(a, rank: int, world: int, dist) -> dict | None:
         plan = sharding.head_shard(shape, world, rank)
     w = DecodeWorkload(dev, layers=a.layers, batch=batch, hq=a.hq, hkv=a.hkv, T=a.ctx, m=a.m, n=a.n,
                        page_tokens=a.page_tokens, seed=rank, plan=plan)
+    from paper_2502_00527_b200 import _lib as _l
+
+    w.base_flags = {"auto": 0, "lut": _l.PQB_DECODE_LUT, "dq": _l.PQB_DECODE_DQ}[a.variant]
     if a.profile:
         with torch.cuda.stream(w.stream):
             for _ in range(max(1, a.steps)):
@@ -367,7 +373,9 @@ def run_ours(a, rank: int, world: int, dist) -> dict | None:
             "unit": "GB/s",
             "frac": achieved / pk["hbm_gbs"],
             "peak_source": pk["source"],
-            "kernel": f"decode_fast_kernel<G={G},M={a.m},N={a.n}> (persistent; timed with the in-kernel split merge disabled)",
+            "kernel": (f"decode_fast_kernel<G={G},M={a.m},N={a.n}> (LUT gather" if a.variant == "lut" or G not in (4, 8)
+                       else f"decode_dq_kernel<G={G},M={a.m},N={a.n}> (product-table gather + tensor-core QK")
+                      + "; persistent; timed with the in-kernel split merge disabled)",
             "algorithmic_bytes_per_launch": algo,
             "avg_launch_ms": ms_attn_layer,
             "step_frac": a.layers * algo / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"],

@@ -8,6 +8,7 @@ or no CUDA device is visible, the product API raises.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -16,7 +17,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libpqb200.so"
 PQB_OK, PQB_EINVAL, PQB_ESTATE, PQB_ECUDA, PQB_EUNSUPPORTED = 0, 1, 2, 3, 4
 PQB_FLAG_NONFINITE, PQB_FLAG_SCALE_OVERFLOW = 1, 2
 PQB_F32, PQB_BF16, PQB_F16 = 0, 1, 2
-PQB_DECODE_FORCE_GENERIC, PQB_DECODE_NO_COMBINE = 1, 2
+PQB_DECODE_FORCE_GENERIC, PQB_DECODE_NO_COMBINE, PQB_DECODE_DQ, PQB_DECODE_LUT = 1, 2, 4, 8
 
 c_i32, c_i64, c_u64, c_f32, c_f64, c_sz = (
     ctypes.c_int32,
@@ -137,7 +138,8 @@ def load(path: Path | str | None = None) -> ctypes.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # PQB_LIB: load another build of the same ABI (A/B timing of kernel variants)
+        p = Path(path) if path else Path(os.environ.get("PQB_LIB", LIB_PATH))
         if not p.exists():
             raise RuntimeError(
                 f"{p} is missing: build the CUDA extension with "

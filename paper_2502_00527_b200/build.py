@@ -24,7 +24,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "pqb200"
 LIB = PKG / "libpqb200.so"
-SOURCES = ["encode.cu", "decode.cu", "misc.cu", "abi.cu"]
+SOURCES = ["encode.cu", "decode.cu", "decode_dq.cu", "misc.cu", "abi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3",
@@ -58,11 +58,15 @@ def _gen_tables() -> None:
     subprocess.run([sys.executable, str(CSRC / "gen_tables.py"), str(CSRC / "angle_tables.h")], check=True)
 
 
-def build(force: bool = False, verbose_ptxas: bool = False, jobs: int | None = None) -> Path:
+def build(force: bool = False, verbose_ptxas: bool = False, jobs: int | None = None,
+          defines: tuple[str, ...] = (), out: Path | None = None) -> Path:
+    """Compile + link libpqb200.so.  defines / out build an A/B variant of the
+    library elsewhere (e.g. build_ab/) without touching the in-tree one."""
     _gen_tables()
     BUILD.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
-    flags = ARCH + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose_ptxas else [])
+    flags = ARCH + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose_ptxas else []) + [f"-D{d}" for d in defines]
+    lib = Path(out) if out is not None else LIB
     objs: list[Path] = []
     todo: list[tuple[Path, Path, Path]] = []
     for name in SOURCES:
@@ -87,19 +91,20 @@ def build(force: bool = False, verbose_ptxas: bool = False, jobs: int | None = N
                     raise RuntimeError(f"nvcc failed on {src.name}:\n{out}")
                 if verbose_ptxas:
                     print(out)
-    if force or todo or not LIB.exists() or any(o.stat().st_mtime > LIB.stat().st_mtime for o in objs):
-        tmp = LIB.with_suffix(".so.tmp")
+    if force or todo or not lib.exists() or any(o.stat().st_mtime > lib.stat().st_mtime for o in objs):
+        lib.parent.mkdir(parents=True, exist_ok=True)
+        tmp = lib.with_suffix(".so.tmp")
         cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}{res.stderr}")
-        os.replace(tmp, LIB)
-    # drop stale objects of older source versions
-    keep = {o.name for o in objs}
-    for o in BUILD.glob("*.o"):
-        if o.name not in keep:
-            o.unlink()
-    return LIB
+        os.replace(tmp, lib)
+    if out is None:  # drop stale objects of older source versions
+        keep = {o.name for o in objs}
+        for o in BUILD.glob("*.o"):
+            if o.name not in keep:
+                o.unlink()
+    return lib
 
 
 def main() -> None:

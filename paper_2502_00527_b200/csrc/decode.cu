@@ -30,175 +30,13 @@
 //   writes a segment partial (m, l, o) and the last CTA to finish the unit
 //   (atomic counter in the workspace) LSE-merges the partials -- one launch per
 //   decode call.
-#include "common.cuh"
+#include "decode_common.cuh"
 #include "kernels.h"
 
 #include <algorithm>
 
 namespace pqb {
 
-constexpr int kNW = 8;      // compute warps per CTA
-constexpr int kStages = 2;  // TMA ring depth per warp
-constexpr int kTile = 32;   // tokens per tile (one per lane)
-constexpr float kLog2e = 1.4426950408889634f;
-constexpr double kPiD = 3.141592653589793115997963468544185161590576171875;  // == np.pi
-constexpr uint32_t kMagic = 0x4B000000u;  // 2^23 as float bits
-
-PQB_DEV const uint8_t* page_base_c(const pqb_store& s, int64_t unit, int64_t page) {
-  const int64_t pid = s.page_table ? static_cast<int64_t>(__ldg(s.page_table + unit * s.max_pages + page))
-                                   : unit * s.max_pages + page;
-  return s.pool + pid * s.page_bytes;
-}
-
-// angle_grid (polar_codec.py:224-233) then cos/sin cast to fp32 (lut_decode.py:69-73).
-PQB_DEV void angle_unit(int m, int a, float& c, float& s) {
-  const double hl = static_cast<double>(1 << (m - 1));
-  const double g = __dsub_rn(__ddiv_rn(__dmul_rn(kPiD, static_cast<double>(a)), hl), kPiD);
-  c = __double2float_rn(cos(g));
-  s = __double2float_rn(sin(g));
-}
-
-PQB_DEV float load_q(const void* q, int dt, int64_t i) {
-  return dt == PQB_F32 ? load1<PQB_F32>(q, i) : (dt == PQB_BF16 ? load1<PQB_BF16>(q, i) : load1<PQB_F16>(q, i));
-}
-
-PQB_DEV uint32_t shift_lr(uint32_t x, int s) { return s >= 0 ? (x >> s) : (x << (-s)); }
-
-// ---- code extraction.  A token's 64 codes of B bits are 2B words (stream
-// bits, LSB first).  For B in {2, 4} the codes are first masked into byte lanes
-// (scaled by 2^S); afterwards each code is one PRMT.
-
-template <int B, int S>
-struct CodeLanes {
-  static constexpr int kMasked = (B == 4 || B == 2) ? 16 : 1;
-  uint32_t mw[kMasked];
-  PQB_DEV void init(const uint32_t* w) {
-    if constexpr (B == 4) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        mw[2 * i] = shift_lr(w[i], -S) & (0x0F0F0F0Fu << S);         // even codes: byte k = code 2k
-        mw[2 * i + 1] = shift_lr(w[i], 4 - S) & (0x0F0F0F0Fu << S);  // odd codes
-      }
-    } else if constexpr (B == 2) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int r = 0; r < 4; ++r) mw[4 * i + r] = shift_lr(w[i], 2 * r - S) & (0x03030303u << S);
-    }
-  }
-  // code j << S, as a register usable as an address offset
-  PQB_DEV uint32_t get(const uint32_t* w, int j) const {
-    if constexpr (B == 4) {
-      return __byte_perm(mw[2 * (j >> 3) + (j & 1)], 0u, 0x4440u | ((j & 7) >> 1));
-    } else if constexpr (B == 2) {
-      return __byte_perm(mw[4 * (j >> 4) + (j & 3)], 0u, 0x4440u | ((j & 15) >> 2));
-    } else {
-      const int bit = j * B, wi = bit >> 5, sh = bit & 31;
-      uint32_t v;
-      if (sh + B <= 32) v = shift_lr(w[wi], sh - S);
-      else v = __funnelshift_r(w[wi], w[wi + 1], sh) << S;
-      return v & (((1u << B) - 1u) << S);
-    }
-  }
-  // float(code j), exact (requires S == 0)
-  PQB_DEV float as_float(const uint32_t* w, int j) const {
-    uint32_t bits;
-    if constexpr (B == 4) {
-      bits = __byte_perm(mw[2 * (j >> 3) + (j & 1)], kMagic, 0x7650u | ((j & 7) >> 1));
-    } else if constexpr (B == 2) {
-      bits = __byte_perm(mw[4 * (j >> 4) + (j & 3)], kMagic, 0x7650u | ((j & 15) >> 2));
-    } else {
-      bits = get(w, j) | kMagic;
-    }
-    return __uint_as_float(bits) - 8388608.0f;
-  }
-};
-
-// A token's 8B code bytes from the stage (lane-strided rows of 8B bytes).  For
-// B = 4 (32-byte rows) the two 16-byte halves are read in lane-dependent order
-// so a quarter-warp's LDS.128 touches 8 distinct bank groups (no 2-way conflict).
-template <int B>
-PQB_DEV void load_token_codes(const uint8_t* row, int lane, uint32_t* w) {
-  if constexpr (B == 4) {
-    const uint32_t sw = (lane >> 2) & 1u;
-    const uint4 v0 = *reinterpret_cast<const uint4*>(row + (sw << 4));
-    const uint4 v1 = *reinterpret_cast<const uint4*>(row + ((sw ^ 1u) << 4));
-    const uint4 lo = sw ? v1 : v0, hi = sw ? v0 : v1;
-    w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
-    w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
-  } else {
-    const uint2* p = reinterpret_cast<const uint2*>(row);
-#pragma unroll
-    for (int i = 0; i < B; ++i) {
-      const uint2 v = p[i];
-      w[2 * i] = v.x;
-      w[2 * i + 1] = v.y;
-    }
-  }
-}
-
-// ---- tensor-core helpers
-
-PQB_DEV void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-
-PQB_DEV void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
-      "{%0, %1, %2, %3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-// ------------------------------------------------------------------ epilogue
-
-struct EpiArgs {
-  void* out;
-  int out_dtype;
-  float* part_ml;  // [n_units][slots][G][2]
-  float* part_o;   // [n_units][slots][G][d]
-  int* counters;   // [n_units] finished-segment counts (zero between calls)
-  int slots;       // partial slots per unit
-  bool merge;      // fast kernel: last CTA of a unit merges (else leave partials)
-};
-
-PQB_DEV void store_out(void* out, int dt, int64_t idx, float v) {
-  if (dt == PQB_F32) static_cast<float*>(out)[idx] = v;
-  else static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
-}
-
-// Persistent work split: items = n_units * tiles_max, CTA c owns
-// [c*per_cta, min(items, (c+1)*per_cta)).  The slot of (unit u, CTA c) is
-// c - first_cta(u).
-struct WorkSplit {
-  int64_t items, per_cta;
-  int tiles_max;
-};
-
-PQB_DEV int64_t first_cta(const WorkSplit& w, int64_t unit) { return (unit * w.tiles_max) / w.per_cta; }
-PQB_DEV int64_t last_cta(const WorkSplit& w, int64_t unit) { return ((unit + 1) * w.tiles_max - 1) / w.per_cta; }
-
-// LSE merge of a unit's segment partials: out = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M)
-PQB_DEV void merge_slots(const EpiArgs& ep, int64_t unit, int nseg, int G, int tid, int nthreads) {
-  for (int i = tid; i < G * 128; i += nthreads) {
-    const int g = i >> 7, e = i & 127;
-    float mx = -INFINITY;
-    for (int s = 0; s < nseg; ++s) mx = fmaxf(mx, __ldcg(ep.part_ml + 2 * ((unit * ep.slots + s) * G + g)));
-    float L = 0.0f, O = 0.0f;
-    for (int s = 0; s < nseg; ++s) {
-      const int64_t sl = (unit * ep.slots + s) * G + g;
-      const float ms = __ldcg(ep.part_ml + 2 * sl);
-      if (ms == -INFINITY) continue;
-      const float sc = exp2f(ms - mx);
-      L = fmaf(__ldcg(ep.part_ml + 2 * sl + 1), sc, L);
-      O = fmaf(__ldcg(ep.part_o + sl * 128 + e), sc, O);
-    }
-    store_out(ep.out, ep.out_dtype, (unit * G + g) * 128 + e, O / L);
-  }
-}
 
 // ------------------------------------------------------------------ fast kernel
 
@@ -245,7 +83,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     for (int s = 0; s < kStages; ++s) mbar_init(bar + s, 1);
     fence_mbar_init();
   }
-  const int64_t P = c.store.page_tokens;
+  const int tpp = c.store.page_tokens / kTile;  // tiles per page
   const int64_t i_begin = static_cast<int64_t>(blockIdx.x) * ws.per_cta;
   const int64_t i_end = min(ws.items, i_begin + ws.per_cta);
   uint32_t k_iter = 0;  // per-warp ring position, continues across segments
@@ -264,8 +102,9 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     const int n_tiles = (T + kTile - 1) / kTile;
     const int t_hi = min(static_cast<int>(seg_end - unit * ws.tiles_max), n_tiles);
 
-    // ---- unit setup: query rows, angle table, LUT (+ radius table)
     __syncthreads();  // previous segment finished with LUT / merge area
+    const int first = t_lo + warp;
+    // ---- unit setup: query rows, angle table, LUT (+ radius table)
     for (int i = tid; i < G * 128; i += blockDim.x) q_s[i] = load_q(q, q_dtype, unit * G * 128 + i);
     if (tid < (1 << M)) angle_unit(M, tid, cs_s[tid], cs_s[16 + tid]);
     if constexpr (EXACT) {
@@ -297,32 +136,20 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     }
     __syncthreads();
 
-    // ---- TMA producer: lane 0 of each warp feeds its own ring
-    auto issue = [&](int tile, uint32_t s) {
-      uint8_t* st = my_area + s * Cfg::kStageBytes;
-      const int64_t tok0 = static_cast<int64_t>(tile) * kTile;
-      const int64_t page = tok0 / P, in_page = tok0 - page * P;
-      const uint8_t* pb = page_base_c(c.store, unit, page);
-      const uint32_t bytes = Cfg::kABytes + Cfg::kRBytes + (want_out ? Cfg::kVBytes : 0);
-      mbar_arrive_expect_tx(bar + s, bytes);
-      bulk_g2s(st, pb + c.store.angle_off + in_page * 8 * M, Cfg::kABytes, bar + s);
-      bulk_g2s(st + Cfg::kABytes, pb + c.store.radius_off + in_page * 8 * N, Cfg::kRBytes, bar + s);
-      if (want_out)
-        bulk_g2s(st + Cfg::kABytes + Cfg::kRBytes, pb + c.store.value_off + in_page * 256, Cfg::kVBytes, bar + s);
-    };
-    const int first = t_lo + warp;
+    // ---- lane 0 fills this warp's ring with its first tiles (after the LUT
+    // build: measured faster than overlapping it, scripts/ab_probe.sh)
     if (lane == 0) {
 #pragma unroll
       for (int s = 0; s < kStages; ++s) {
         const int tile = first + s * kNW;
         if (tile < t_hi) {
           fence_proxy_async_smem();
-          issue(tile, (k_iter + s) % kStages);
+          const uint32_t sl = (k_iter + s) % kStages;
+          issue_tile<M, N>(my_area + sl * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, tile / tpp), tile,
+                           tpp, want_out, bar + sl);
         }
       }
     }
-    __syncwarp();
-
     float m_run[G], l_run[G];
     float d[8][4];
 #pragma unroll
@@ -337,6 +164,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 
     for (int tile = first; tile < t_hi; tile += kNW, ++k_iter) {
       const uint32_t s = k_iter % kStages;
+      const int nt = tile + kStages * kNW;  // the tile this stage is refilled with
       mbar_wait(bar + s, (k_iter / kStages) & 1);
       const uint8_t* st = my_area + s * Cfg::kStageBytes;
       const int tok = tile * kTile + lane;
@@ -465,12 +293,10 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) {
-        const int nt = tile + kStages * kNW;
-        if (nt < t_hi) {
-          fence_proxy_async_smem();
-          issue(nt, s);
-        }
+      if (lane == 0 && nt < t_hi) {
+        fence_proxy_async_smem();
+        issue_tile<M, N>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, nt / tpp), nt, tpp,
+                         want_out, bar + s);
       }
     }
     if (!want_out) continue;
@@ -500,48 +326,8 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         mine[(2 * t4 + 1) * 132 + 4 + dim + 8] = d[mt][3];
       }
     }
-    __syncthreads();
-    const int64_t c_first = first_cta(ws, unit);
-    const int nseg = static_cast<int>(last_cta(ws, unit) - c_first + 1);
-    const bool direct = nseg == 1;  // this CTA covers the whole unit: write the output
-    const int64_t slot = (unit * ep.slots + (blockIdx.x - c_first)) * G;
-    for (int i = tid; i < G * 128; i += blockDim.x) {
-      const int g = i >> 7, e = i & 127;
-      float mx = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, red[(w * G + g) * 132]);
-      float L = 0.0f, O = 0.0f;
-      if (mx != -INFINITY) {
-#pragma unroll
-        for (int w = 0; w < kNW; ++w) {
-          const float* rw = red + (w * G + g) * 132;
-          const float sc = exp2f(rw[0] - mx);
-          L = fmaf(rw[1], sc, L);
-          O = fmaf(rw[4 + e], sc, O);
-        }
-      }
-      if (direct && ep.merge) {
-        store_out(ep.out, ep.out_dtype, (unit * G + g) * 128 + e, O / L);
-      } else {
-        ep.part_o[(slot + g) * 128 + e] = O;
-        if (e == 0) {
-          ep.part_ml[2 * (slot + g)] = mx;
-          ep.part_ml[2 * (slot + g) + 1] = L;
-        }
-      }
-    }
-    if (direct || !ep.merge) continue;
-    // ---- the last CTA to finish a unit merges its segments (no extra launch)
-    __threadfence();
-    __syncthreads();
     __shared__ int s_last;
-    if (tid == 0) s_last = atomicAdd(ep.counters + unit, 1) == nseg - 1;
-    __syncthreads();
-    if (s_last) {
-      __threadfence();
-      merge_slots(ep, unit, nseg, G, tid, blockDim.x);
-      if (tid == 0) ep.counters[unit] = 0;  // leave the workspace zeroed for the next call
-    }
+    finish_segment<G>(ep, ws, unit, red, &s_last, tid, blockDim.x);
   }
 }
 
@@ -771,6 +557,28 @@ size_t decode_workspace_bytes(int64_t n_units, int group, int max_tokens, int d)
   return counter_bytes(n_units) + partial_bytes(n_units, group, max_tokens, d) + 256;
 }
 
+// Work split + epilogue arguments shared by the LUT and DQ fast kernels.
+static int fast_setup(const DecodeArgs& a, EpiArgs& ep, WorkSplit& ws, int& grid) {
+  const int ctas = a.splits > 0 ? std::min(a.splits, kMaxCtas) : std::min(num_sms(), kMaxCtas);
+  ws = make_split(a.n_units, a.max_tokens, ctas);
+  grid = static_cast<int>((ws.items + ws.per_cta - 1) / ws.per_cta);
+  ep.out = a.out;
+  ep.out_dtype = a.out_dtype;
+  ep.slots = fast_slots(a.n_units, a.max_tokens);
+  ep.counters = static_cast<int*>(a.workspace);
+  ep.part_ml = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + counter_bytes(a.n_units));
+  ep.part_o = ep.part_ml + a.n_units * ep.slots * a.group * 2;
+  ep.merge = !(a.flags & PQB_DECODE_NO_COMBINE);
+  if (a.out != nullptr) {
+    const size_t need = decode_workspace_bytes(a.n_units, a.group, a.max_tokens, 128);
+    if (a.workspace == nullptr || a.workspace_bytes < need) {
+      set_error("decode workspace too small: need %zu bytes, got %zu", need, a.workspace_bytes);
+      return PQB_EINVAL;
+    }
+  }
+  return PQB_OK;
+}
+
 template <int G, int M, int N, bool EXACT>
 static int launch_fast(const DecodeArgs& a, cudaStream_t s) {
   using Cfg = FastCfg<G, M, N, EXACT>;
@@ -783,27 +591,37 @@ static int launch_fast(const DecodeArgs& a, cudaStream_t s) {
     }
     attr_set = true;
   }
-  const int ctas = a.splits > 0 ? std::min(a.splits, kMaxCtas) : std::min(num_sms(), kMaxCtas);
-  const WorkSplit ws = make_split(a.n_units, a.max_tokens, ctas);
-  const int grid = static_cast<int>((ws.items + ws.per_cta - 1) / ws.per_cta);
   EpiArgs ep;
-  ep.out = a.out;
-  ep.out_dtype = a.out_dtype;
-  ep.slots = fast_slots(a.n_units, a.max_tokens);
-  ep.counters = static_cast<int*>(a.workspace);
-  ep.part_ml = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + counter_bytes(a.n_units));
-  ep.part_o = ep.part_ml + a.n_units * ep.slots * G * 2;
-  ep.merge = !(a.flags & PQB_DECODE_NO_COMBINE);
-  if (a.out != nullptr) {
-    const size_t need = decode_workspace_bytes(a.n_units, a.group, a.max_tokens, 128);
-    if (a.workspace == nullptr || a.workspace_bytes < need) {
-      set_error("decode workspace too small: need %zu bytes, got %zu", need, a.workspace_bytes);
-      return PQB_EINVAL;
-    }
-  }
+  WorkSplit ws;
+  int grid = 0;
+  const int rc = fast_setup(a, ep, ws, grid);
+  if (rc != PQB_OK) return rc;
   decode_fast_kernel<G, M, N, EXACT><<<grid, kNW * 32, Cfg::kSmem, s>>>(
       *a.cache, a.q, a.q_dtype, a.sm_scale * kLog2e, a.scores, a.scores_ld, ep, ws);
   return PQB_OK;
+}
+
+// Scoring variant for the fused (output-only) call.  G in {4, 8}: the product-
+// table gather + tensor-core contraction of decode_dq.cu (A/B on B200,
+// configs[1] launch: 0.87 vs 0.80 of HBM peak at G = 4, 0.66 vs 0.45 at G = 8;
+// the LUT gather is shared-memory bound).  Scores requested, G = 1 or
+// PQB_DECODE_LUT: the LUT kernel (bit-exact qk_scores sequence).
+static bool use_dq(const DecodeArgs& a) {
+  if (a.scores != nullptr || a.out == nullptr || (a.group != 4 && a.group != 8)) return false;
+  if (a.flags & PQB_DECODE_LUT) return false;
+  return true;
+}
+
+static int launch_dq_path(const DecodeArgs& a, cudaStream_t s, bool& handled) {
+  EpiArgs ep;
+  WorkSplit ws;
+  int grid = 0;
+  const int rc = fast_setup(a, ep, ws, grid);
+  if (rc != PQB_OK) {
+    handled = true;
+    return rc;
+  }
+  return launch_decode_dq(a, ep, ws, grid, s, handled);
 }
 
 template <int G, bool EXACT>
@@ -835,7 +653,11 @@ int launch_decode(const DecodeArgs& a, cudaStream_t s) {
                        (c.store.value_off % 16 == 0 || a.out == nullptr) && (c.store.page_bytes % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(c.store.pool) % 16 == 0);
   bool handled = false;
-  if (fast_ok && !(a.flags & PQB_DECODE_FORCE_GENERIC)) {
+  if (fast_ok && !(a.flags & PQB_DECODE_FORCE_GENERIC) && use_dq(a)) {
+    const int rc = launch_dq_path(a, s, handled);
+    if (rc != PQB_OK) return rc;
+  }
+  if (fast_ok && !handled && !(a.flags & PQB_DECODE_FORCE_GENERIC)) {
     // scores requested -> the bit-exact scoring sequence; fused-only -> FMA form
     const int rc = a.scores != nullptr ? dispatch_fast<true>(a, s, handled) : dispatch_fast<false>(a, s, handled);
     if (rc != PQB_OK) return rc;

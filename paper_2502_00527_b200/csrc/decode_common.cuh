@@ -1,0 +1,246 @@
+// Shared pieces of the decode kernels (LUT: decode.cu, dequant + tensor-core
+// scoring: decode_dq.cu): constants, code extraction, mma helpers, the
+// persistent work split and the segment epilogue (warp merge, direct output or
+// partial + last-CTA merge).
+#pragma once
+
+#include "common.cuh"
+
+namespace pqb {
+
+constexpr int kNW = 8;      // compute warps per CTA
+constexpr int kStages = 2;  // TMA ring depth per warp
+constexpr int kTile = 32;   // tokens per tile (one per lane)
+constexpr float kLog2e = 1.4426950408889634f;
+constexpr double kPiD = 3.141592653589793115997963468544185161590576171875;  // == np.pi
+constexpr uint32_t kMagic = 0x4B000000u;  // 2^23 as float bits
+
+PQB_DEV const uint8_t* page_base_c(const pqb_store& s, int64_t unit, int64_t page) {
+  const int64_t pid = s.page_table ? static_cast<int64_t>(__ldg(s.page_table + unit * s.max_pages + page))
+                                   : unit * s.max_pages + page;
+  return s.pool + pid * s.page_bytes;
+}
+
+// angle_grid (polar_codec.py:224-233) then cos/sin cast to fp32 (lut_decode.py:69-73).
+PQB_DEV void angle_unit(int m, int a, float& c, float& s) {
+  const double hl = static_cast<double>(1 << (m - 1));
+  const double g = __dsub_rn(__ddiv_rn(__dmul_rn(kPiD, static_cast<double>(a)), hl), kPiD);
+  c = __double2float_rn(cos(g));
+  s = __double2float_rn(sin(g));
+}
+
+PQB_DEV float load_q(const void* q, int dt, int64_t i) {
+  return dt == PQB_F32 ? load1<PQB_F32>(q, i) : (dt == PQB_BF16 ? load1<PQB_BF16>(q, i) : load1<PQB_F16>(q, i));
+}
+
+PQB_DEV uint32_t shift_lr(uint32_t x, int s) { return s >= 0 ? (x >> s) : (x << (-s)); }
+
+// ---- code extraction.  A token's 64 codes of B bits are 2B words (stream
+// bits, LSB first).  For B in {2, 4} the codes are first masked into byte lanes
+// (scaled by 2^S); afterwards each code is one PRMT.
+
+template <int B, int S>
+struct CodeLanes {
+  static constexpr int kMasked = (B == 4 || B == 2) ? 16 : 1;
+  uint32_t mw[kMasked];
+  PQB_DEV void init(const uint32_t* w) {
+    if constexpr (B == 4) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        mw[2 * i] = shift_lr(w[i], -S) & (0x0F0F0F0Fu << S);         // even codes: byte k = code 2k
+        mw[2 * i + 1] = shift_lr(w[i], 4 - S) & (0x0F0F0F0Fu << S);  // odd codes
+      }
+    } else if constexpr (B == 2) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) mw[4 * i + r] = shift_lr(w[i], 2 * r - S) & (0x03030303u << S);
+    }
+  }
+  // code j << S, as a register usable as an address offset
+  PQB_DEV uint32_t get(const uint32_t* w, int j) const {
+    if constexpr (B == 4) {
+      return __byte_perm(mw[2 * (j >> 3) + (j & 1)], 0u, 0x4440u | ((j & 7) >> 1));
+    } else if constexpr (B == 2) {
+      return __byte_perm(mw[4 * (j >> 4) + (j & 3)], 0u, 0x4440u | ((j & 15) >> 2));
+    } else {
+      const int bit = j * B, wi = bit >> 5, sh = bit & 31;
+      uint32_t v;
+      if (sh + B <= 32) v = shift_lr(w[wi], sh - S);
+      else v = __funnelshift_r(w[wi], w[wi + 1], sh) << S;
+      return v & (((1u << B) - 1u) << S);
+    }
+  }
+  // float(code j), exact (requires S == 0)
+  PQB_DEV float as_float(const uint32_t* w, int j) const {
+    uint32_t bits;
+    if constexpr (B == 4) {
+      bits = __byte_perm(mw[2 * (j >> 3) + (j & 1)], kMagic, 0x7650u | ((j & 7) >> 1));
+    } else if constexpr (B == 2) {
+      bits = __byte_perm(mw[4 * (j >> 4) + (j & 3)], kMagic, 0x7650u | ((j & 15) >> 2));
+    } else {
+      bits = get(w, j) | kMagic;
+    }
+    return __uint_as_float(bits) - 8388608.0f;
+  }
+};
+
+// A token's 8B code bytes from the stage (lane-strided rows of 8B bytes).  For
+// B = 4 (32-byte rows) the two 16-byte halves are read in lane-dependent order
+// so a quarter-warp's LDS.128 touches 8 distinct bank groups (no 2-way conflict).
+template <int B>
+PQB_DEV void load_token_codes(const uint8_t* row, int lane, uint32_t* w) {
+  if constexpr (B == 4) {
+    const uint32_t sw = (lane >> 2) & 1u;
+    const uint4 v0 = *reinterpret_cast<const uint4*>(row + (sw << 4));
+    const uint4 v1 = *reinterpret_cast<const uint4*>(row + ((sw ^ 1u) << 4));
+    const uint4 lo = sw ? v1 : v0, hi = sw ? v0 : v1;
+    w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w;
+    w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
+  } else {
+    const uint2* p = reinterpret_cast<const uint2*>(row);
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const uint2 v = p[i];
+      w[2 * i] = v.x;
+      w[2 * i + 1] = v.y;
+    }
+  }
+}
+
+// ---- tensor-core helpers
+
+PQB_DEV void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+
+PQB_DEV void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// ---- TMA producer.  One tile = angle codes (32 * 8M B), radius codes (32 * 8N B)
+// and optionally the bf16 value rows (8 KB) of 32 consecutive tokens of one page
+// (tpp = tiles per page).  The caller resolves the page base (page-table load)
+// one tile ahead so its latency is off the issue path.
+template <int M, int N>
+PQB_DEV void issue_tile(uint8_t* st, const pqb_store& s, const uint8_t* pb, int tile, int tpp, bool with_v,
+                        uint64_t* bar) {
+  constexpr uint32_t kA = kTile * 8 * M, kR = kTile * 8 * N, kV = kTile * 256;
+  const int in_page = (tile % tpp) * kTile;
+  mbar_arrive_expect_tx(bar, kA + kR + (with_v ? kV : 0u));
+  bulk_g2s(st, pb + s.angle_off + in_page * 8 * M, kA, bar);
+  bulk_g2s(st + kA, pb + s.radius_off + in_page * 8 * N, kR, bar);
+  if (with_v) bulk_g2s(st + kA + kR, pb + s.value_off + static_cast<int64_t>(in_page) * 256, kV, bar);
+}
+
+// ------------------------------------------------------------------ epilogue
+
+struct EpiArgs {
+  void* out;
+  int out_dtype;
+  float* part_ml;  // [n_units][slots][G][2]
+  float* part_o;   // [n_units][slots][G][d]
+  int* counters;   // [n_units] finished-segment counts (zero between calls)
+  int slots;       // partial slots per unit
+  bool merge;      // fast kernel: last CTA of a unit merges (else leave partials)
+};
+
+PQB_DEV void store_out(void* out, int dt, int64_t idx, float v) {
+  if (dt == PQB_F32) static_cast<float*>(out)[idx] = v;
+  else static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
+}
+
+// Persistent work split: items = n_units * tiles_max, CTA c owns
+// [c*per_cta, min(items, (c+1)*per_cta)).  The slot of (unit u, CTA c) is
+// c - first_cta(u).
+struct WorkSplit {
+  int64_t items, per_cta;
+  int tiles_max;
+};
+
+PQB_DEV int64_t first_cta(const WorkSplit& w, int64_t unit) { return (unit * w.tiles_max) / w.per_cta; }
+PQB_DEV int64_t last_cta(const WorkSplit& w, int64_t unit) { return ((unit + 1) * w.tiles_max - 1) / w.per_cta; }
+
+// LSE merge of a unit's segment partials: out = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M)
+PQB_DEV void merge_slots(const EpiArgs& ep, int64_t unit, int nseg, int G, int tid, int nthreads) {
+  for (int i = tid; i < G * 128; i += nthreads) {
+    const int g = i >> 7, e = i & 127;
+    float mx = -INFINITY;
+    for (int s = 0; s < nseg; ++s) mx = fmaxf(mx, __ldcg(ep.part_ml + 2 * ((unit * ep.slots + s) * G + g)));
+    float L = 0.0f, O = 0.0f;
+    for (int s = 0; s < nseg; ++s) {
+      const int64_t sl = (unit * ep.slots + s) * G + g;
+      const float ms = __ldcg(ep.part_ml + 2 * sl);
+      if (ms == -INFINITY) continue;
+      const float sc = exp2f(ms - mx);
+      L = fmaf(__ldcg(ep.part_ml + 2 * sl + 1), sc, L);
+      O = fmaf(__ldcg(ep.part_o + sl * 128 + e), sc, O);
+    }
+    store_out(ep.out, ep.out_dtype, (unit * G + g) * 128 + e, O / L);
+  }
+}
+
+// End of a unit segment.  Every warp has written, for each query g, its running
+// max, its row sum and its 128 output accumulators into red[warp][g][132]
+// (m, l, pad, pad, o[128]).  Merge the warps; a CTA covering the whole unit
+// stores the output, otherwise it writes a partial slot and the last CTA to
+// finish the unit LSE-merges the slots.  Caller: all threads, after the
+// red writes (this function starts with a __syncthreads()).
+template <int G>
+PQB_DEV void finish_segment(const EpiArgs& ep, const WorkSplit& ws, int64_t unit, const float* red, int* s_flag,
+                            int tid, int nthreads) {
+  __syncthreads();
+  const int64_t c_first = first_cta(ws, unit);
+  const int nseg = static_cast<int>(last_cta(ws, unit) - c_first + 1);
+  const bool direct = nseg == 1;
+  const int64_t slot = (unit * ep.slots + (blockIdx.x - c_first)) * G;
+  for (int i = tid; i < G * 128; i += nthreads) {
+    const int g = i >> 7, e = i & 127;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, red[(w * G + g) * 132]);
+    float L = 0.0f, O = 0.0f;
+    if (mx != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kNW; ++w) {
+        const float* rw = red + (w * G + g) * 132;
+        const float sc = exp2f(rw[0] - mx);
+        L = fmaf(rw[1], sc, L);
+        O = fmaf(rw[4 + e], sc, O);
+      }
+    }
+    if (direct && ep.merge) {
+      store_out(ep.out, ep.out_dtype, (unit * G + g) * 128 + e, O / L);
+    } else {
+      ep.part_o[(slot + g) * 128 + e] = O;
+      if (e == 0) {
+        ep.part_ml[2 * (slot + g)] = mx;
+        ep.part_ml[2 * (slot + g) + 1] = L;
+      }
+    }
+  }
+  if (direct || !ep.merge) return;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) *s_flag = atomicAdd(ep.counters + unit, 1) == nseg - 1;
+  __syncthreads();
+  if (*s_flag) {
+    __threadfence();
+    merge_slots(ep, unit, nseg, G, tid, nthreads);
+    if (tid == 0) ep.counters[unit] = 0;  // leave the workspace zeroed for the next call
+  }
+}
+
+struct DecodeArgs;
+// decode_dq.cu: dequantize + tensor-core scoring variant of the fused kernel
+// (G in {4, 8}, fused output only).  handled = false when (m, n) has no instance.
+int launch_decode_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s,
+                     bool& handled);
+
+}  // namespace pqb

@@ -254,3 +254,64 @@ def test_views_and_workspace_reuse():
             s16 = cache.scales16[upl + u].cpu().numpy()
             ref = po.softmax64(exact.lut_scores(q8[u, 3].cpu().numpy(), a, r, s16, 4, 4, 1), 1 / math.sqrt(128))
             peak_close(o8[u, 3], ref @ vb[upl + u], OUT_RTOL_F32)
+
+
+@pytest.mark.parametrize("m,n", [(4, 4), (3, 2), (2, 2), (4, 2), (2, 4), (3, 4)])
+@pytest.mark.parametrize("G", [4, 8])
+@pytest.mark.parametrize("lay,res", [(1, 0), (0, 0), (1, 40)])
+def test_dq_decode_vs_oracle(m, n, G, lay, res):
+    """Dequantize + tensor-core scoring kernel (decode_dq.cu): fused output
+    within the fp32 tolerance of softmax64(exact LUT scores) . V, both layouts,
+    residual windows, ragged lengths."""
+    U = 3
+    lens = [3000, 1777, 33]
+    T = max(lens)
+    keys = [po.synthetic_keys(t, 128, seed=700 + u, outliers=(0, 1), layout=lay) for u, t in enumerate(lens)]
+    rng = np.random.default_rng(m * 10 + n + G)
+    vals = [rng.standard_normal((t, 128)).astype(np.float32) for t in lens]
+    q = rng.standard_normal((U, G, 128)).astype(np.float32)
+    cache = pq.PolarKVCache(pq.QuantConfig(m, n, LAY[lay]), U, 128, res, capacity=T + 1)
+    for u in range(U):
+        cache.prefill(torch.from_numpy(keys[u]).cuda().unsqueeze(0), torch.from_numpy(vals[u]).cuda().unsqueeze(0),
+                      unit_start=u)
+    qd = torch.from_numpy(q).cuda()
+    out = cache.decode(qd, flags=pq._lib.PQB_DECODE_DQ).cpu().numpy()
+    lut = cache.decode(qd, flags=pq._lib.PQB_DECODE_LUT).cpu().numpy()
+    for u in range(U):
+        a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
+        s16 = cache.scales16[u].cpu().numpy()
+        vb = torch.from_numpy(vals[u]).to(torch.bfloat16).float().numpy().astype(np.float64)
+        t_u = lens[u]
+        resid = keys[u][t_u - min(res, t_u):] if res else np.zeros((0, 128), np.float32)
+        for g in range(G):
+            ref = po.lut_scores(q[u, g], a, r, s16, m, n, lay, resid)
+            o_ref = po.softmax64(ref, 1.0 / math.sqrt(128)) @ vb
+            peak_close(out[u, g], o_ref, OUT_RTOL_F32)
+            peak_close(lut[u, g], o_ref, OUT_RTOL_F32)
+    if G == 8:  # the default fused path for G = 8 is the DQ kernel
+        assert np.array_equal(cache.decode(qd).cpu().numpy(), out)
+
+
+def test_dq_extreme_scales_and_zero_query():
+    """Q' normalisation (2^e) with tiny / huge channel scales, dead channels and
+    an all-zero query row."""
+    U, T, G = 2, 700, 8
+    rng = np.random.default_rng(3)
+    keys = rng.standard_normal((U, T, 128)).astype(np.float32)
+    keys[0] *= 1e-3
+    keys[1] *= 300.0
+    keys[:, :, 5] = 0.0
+    keys[:, :, 69] = 0.0  # pair 5 dead in HALF_SPLIT -> scale 0
+    vals = rng.standard_normal((U, T, 128)).astype(np.float32)
+    q = rng.standard_normal((U, G, 128)).astype(np.float32)
+    q[1, 2] = 0.0
+    cache = pq.PolarKVCache(pq.QuantConfig(4, 4), U, 128, 0, capacity=T)
+    cache.prefill(torch.from_numpy(keys).cuda(), torch.from_numpy(vals).cuda())
+    out = cache.decode(torch.from_numpy(q).cuda(), flags=pq._lib.PQB_DECODE_DQ).cpu().numpy()
+    for u in range(U):
+        a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
+        s16 = cache.scales16[u].cpu().numpy()
+        vb = torch.from_numpy(vals[u]).to(torch.bfloat16).float().numpy().astype(np.float64)
+        for g in range(G):
+            ref = exact.lut_scores(q[u, g], a, r, s16, 4, 4, 1)
+            peak_close(out[u, g], po.softmax64(ref, 1.0 / math.sqrt(128)) @ vb, OUT_RTOL_F32)
