@@ -185,6 +185,8 @@ int pqb_decode_attn(const pqb_cache* cache, int64_t n_units, int group, const vo
 #define PQB_DECODE_NO_COMBINE 2    /* leave split partials in the workspace (timing) */
 #define PQB_DECODE_DQ 4            /* fused call: product-table + tensor-core scoring (default, G 4/8) */
 #define PQB_DECODE_LUT 8           /* fused call: LUT-gather scoring (default for scores / G = 1)     */
+#define PQB_DECODE_PROBE_MEM 64    /* diagnostics, m4n4 DQ only: stream tiles, skip all compute      */
+#define PQB_DECODE_PROBE_COMPUTE 128 /* diagnostics, m4n4 DQ only: compute on L2-resident tiles      */
 int pqb_decode_attn_ex(const pqb_cache* cache, int64_t n_units, int group, const void* q,
                        int q_dtype, float sm_scale, int max_tokens, void* out, int out_dtype,
                        float* scores, int64_t scores_ld, void* workspace, size_t workspace_bytes,

@@ -55,18 +55,18 @@ struct DqCfg {
   static constexpr int kRBytes = kTile * 8 * N;
   static constexpr int kVBytes = kTile * 256;
   static constexpr int kStageBytes = kABytes + kRBytes + kVBytes;
-  static constexpr int kPBytes = 2 * kTile * 16;             // bf16 [hi/lo][32 tokens][8 queries]; fp32 [32][8] residual scratch
+  static constexpr int kPBytes = kTile * 8 * 4;              // fp32 [32 tokens][8 queries] residual-dot scratch
   static constexpr int kTabBytes = 128 << (M + N);          // product table, 16 bank-slot copies
-  static constexpr int kFragBytes = 8 * 32 * 16;             // Q' B-fragments [ks][lane] uint4
+  static constexpr int kFragBytes = 16 * 32 * 16;            // Q' A-fragments [ks][lane] uint4 (hi, lo, hi, lo)
   static constexpr int kHeadBytes = kTabBytes + kFragBytes + G * 128 * 4 + 128 + 8 * (1 << M);
   static constexpr int kWarpBytes = kStages * kStageBytes + kPBytes + 64;
   static constexpr int kSmem = kHeadBytes + kNW * kWarpBytes + 128;
+  static constexpr bool kPacked = G <= 4;  // P.V: columns 0-3 carry P_hi, 4-7 P_lo
   static_assert(kHeadBytes % 16 == 0 && kWarpBytes % 16 == 0, "alignment");
   static_assert(kNW * kStages * kStageBytes >= kNW * G * 132 * 4, "merge area");
 };
 
 PQB_DEV uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
-PQB_DEV __half2 bits_h2(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 
 PQB_DEV void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -76,37 +76,110 @@ PQB_DEV void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint3
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// Code i of the lane's pair set {4i + t4} from the row pre-shifted by t4*B bits:
-// it sits at bit 4iB (never straddles a word for B in {2, 3, 4}).
-template <int B>
-PQB_DEV uint32_t dq_code(const uint32_t* ws, int i) {
-  const int bit = 4 * i * B;
-  return (ws[bit >> 5] >> (bit & 31)) & ((1u << B) - 1u);
+// Lane t4 owns channel pairs [16 t4, 16 t4 + 16) of every token; k-step ks
+// contracts pair 16 t4 + dq_pair(ks).  For m = n = 4 the order follows the
+// nibble fusion below (even pairs of a word, then odd), else it is ks.
+template <bool FUSED>
+PQB_DEV constexpr int dq_pair(int ks) {
+  return FUSED ? ((ks >> 2) & 1) + 2 * (ks & 3) + 8 * (ks >> 3) : ks;
 }
 
-// Product-table indices (a << N) | r of codes i and i + 1 (i even).
-template <int M, int N>
-PQB_DEV void dq_index2(const uint32_t* wa, const uint32_t* wr, int i, uint32_t& i0, uint32_t& i1) {
-  if constexpr (M == 4 && N == 4) {
-    // codes i, i+1 at bits 0 and 16 of word i/2 in both streams
-    const uint32_t v = ((wa[i >> 1] << 4) & 0x00F000F0u) | (wr[i >> 1] & 0x000F000Fu);
-    i0 = v & 0xFFu;
-    i1 = v >> 16;
+// B bits starting at bit b of the little-endian word array x (b compile-time
+// after unrolling).
+template <int B>
+PQB_DEV uint32_t bits_at(const uint32_t* x, int b) {
+  const int w = b >> 5, s = b & 31;
+  const uint32_t v = (s + B <= 32) ? (x[w] >> s) : __funnelshift_r(x[w], x[w + 1], s);
+  return v & ((1u << B) - 1u);
+}
+
+// The lane's 16 codes of B bits (stream bits [16 t4 B, 16 t4 B + 16 B) of the
+// token row), right-aligned into x[0..].  16 t4 B is a multiple of 16 bits.
+template <int B>
+PQB_DEV void load_lane_codes(const uint8_t* row, int t4, uint32_t (&x)[(B + 1) / 2 + 1]) {
+  constexpr int kW = (B + 1) / 2 + 1;
+  const int bit0 = 16 * t4 * B;
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row) + (bit0 >> 5);
+  if constexpr (B % 2 == 0) {  // word aligned
+#pragma unroll
+    for (int k = 0; k < B / 2; ++k) x[k] = w[k];
+    x[kW - 1] = 0u;
   } else {
-    i0 = (dq_code<M>(wa, i) << N) | dq_code<N>(wr, i);
-    i1 = (dq_code<M>(wa, i + 1) << N) | dq_code<N>(wr, i + 1);
+    uint32_t r[kW];
+#pragma unroll
+    for (int k = 0; k < kW; ++k) r[k] = w[k];
+    const int sh = bit0 & 31;  // 0 or 16
+#pragma unroll
+    for (int k = 0; k < kW - 1; ++k) x[k] = __funnelshift_r(r[k], r[k + 1], sh);
+    x[kW - 1] = 0u;
   }
 }
 
-template <int G, int M, int N>
+// Product-table indices idx = (a << N) | r of the lane's 16 pairs of one token.
+// For m = n = 4 they stay packed: byte k of w[q] is the index of k-step 4q + k
+// (w = e0, o0, e1, o1 with e = (a_even << 4) | r_even, o = (a_odd << 4) | r_odd);
+// otherwise w[ks] is the index itself.  live = false (a residual or past-the-end
+// token) forces radius code 0, i.e. the zero key.
+template <int M, int N>
+struct DqIdx {
+  static constexpr bool kFused = M == 4 && N == 4;
+  uint32_t w[kFused ? 4 : 16];
+  PQB_DEV void load(const uint8_t* arow, const uint8_t* rrow, int t4, bool live) {
+    if constexpr (kFused) {
+      const uint2 a = *reinterpret_cast<const uint2*>(arow + 8 * t4);
+      uint2 r = *reinterpret_cast<const uint2*>(rrow + 8 * t4);
+      if (!live) r = make_uint2(0u, 0u);
+      w[0] = ((a.x << 4) & 0xF0F0F0F0u) | (r.x & 0x0F0F0F0Fu);
+      w[1] = (a.x & 0xF0F0F0F0u) | ((r.x >> 4) & 0x0F0F0F0Fu);
+      w[2] = ((a.y << 4) & 0xF0F0F0F0u) | (r.y & 0x0F0F0F0Fu);
+      w[3] = (a.y & 0xF0F0F0F0u) | ((r.y >> 4) & 0x0F0F0F0Fu);
+    } else {
+      uint32_t xa[(M + 1) / 2 + 1], xr[(N + 1) / 2 + 1];
+      load_lane_codes<M>(arow, t4, xa);
+      load_lane_codes<N>(rrow, t4, xr);
+      if (!live) {
+#pragma unroll
+        for (int k = 0; k < (N + 1) / 2 + 1; ++k) xr[k] = 0u;
+      }
+#pragma unroll
+      for (int ks = 0; ks < 16; ++ks) w[ks] = (bits_at<M>(xa, ks * M) << N) | bits_at<N>(xr, ks * N);
+    }
+  }
+  // shared address of the k-step ks entry in the lane's table copy
+  PQB_DEV uint32_t addr(uint32_t tab, int ks) const {
+    if constexpr (kFused) return tab + (__byte_perm(w[ks >> 2], 0u, 0x4440u | (ks & 3)) << 7);
+    else return tab + (w[ks] << 7);
+  }
+};
+
+// 2^x on the SFU (ex2.approx.ftz: ~2 ulp, results below 2^-126 flush to 0;
+// exp2f's range fix-up would add three instructions per call)
+PQB_DEV float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+PQB_DEV uint2 lds_u2(uint32_t addr) {
+  uint2 v;
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+
+// PROBE (diagnostics only, flags PQB_DECODE_PROBE_*): 0 = the kernel; 1 = memory
+// only (tiles stream through the ring, no compute); 2 = compute only (every tile
+// is re-read from the unit's first page, i.e. from L2).
+template <int G, int M, int N, int PROBE = 0>
 __global__ void __launch_bounds__(kNW * 32, 1)
     decode_dq_kernel(const pqb_cache c, const void* __restrict__ q, int q_dtype, float sm_scale_log2, EpiArgs ep,
                      WorkSplit ws) {
   using Cfg = DqCfg<G, M, N>;
-  static_assert(G == 4 || G == 8, "G");
+  constexpr bool kFused = M == 4 && N == 4;
+  constexpr bool kPacked = Cfg::kPacked;
+  static_assert(G == 1 || G == 2 || G == 4 || G == 8, "G");
   extern __shared__ __align__(128) uint8_t smem[];
   uint2* ptab = reinterpret_cast<uint2*>(smem);                                   // [2^(M+N)][16]
-  uint4* qfrag = reinterpret_cast<uint4*>(smem + Cfg::kTabBytes);                    // [8][32]
+  uint4* qfrag = reinterpret_cast<uint4*>(smem + Cfg::kTabBytes);                    // [16][32]
   float* q_s = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(qfrag) + Cfg::kFragBytes);  // [G][128]
   int* s_misc = reinterpret_cast<int*>(q_s + G * 128);  // [0] max|Q'| bits, [1] merge flag
   float2* cs_s = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(s_misc) + 128);  // [2^M] (cos, sin)
@@ -114,8 +187,8 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* my_area = warp_area + warp * Cfg::kWarpBytes;
-  uint8_t* pbuf = my_area + kStages * Cfg::kStageBytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(pbuf + Cfg::kPBytes);
+  float* rbuf = reinterpret_cast<float*>(my_area + kStages * Cfg::kStageBytes);  // [32][8]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(my_area + kStages * Cfg::kStageBytes + Cfg::kPBytes);
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(bar + s, 1);
@@ -137,7 +210,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
                          h2_bits(__halves2half2(__float2half_rn(static_cast<float>(x - __half2float(xh))),
                                                 __float2half_rn(static_cast<float>(y - __half2float(yh))))));
   }
-  const uint8_t* ptab_l = smem + ((threadIdx.x & 15) << 3);  // this lane's bank-slot copy
+  const uint32_t ptab_l = smem_u32(smem) + ((lane & 15) << 3);  // this lane's bank-slot copy
   const int tpp = c.store.page_tokens / kTile;  // tiles per page
   const int64_t i_begin = static_cast<int64_t>(blockIdx.x) * ws.per_cta;
   const int64_t i_end = min(ws.items, i_begin + ws.per_cta);
@@ -146,6 +219,8 @@ __global__ void __launch_bounds__(kNW * 32, 1)
   const int g8 = lane >> 2, t4 = lane & 3;  // fragment group / thread-in-group
   const uint32_t ld_row = static_cast<uint32_t>((((lane >> 4) & 1) * 8 + (lane & 7)) * 256);
   const uint32_t ld_chunk = static_cast<uint32_t>((((lane >> 3) & 1) ^ (lane & 7)) << 4);
+  // P.V output columns 2 t4, 2 t4 + 1 belong to queries qc0, qc1 (packed: col & 3)
+  const int qc0 = kPacked ? ((2 * t4) & 3) : 2 * t4, qc1 = qc0 + 1;
 
   for (int64_t seg = i_begin; seg < i_end;) {
     const int64_t unit = seg / ws.tiles_max;
@@ -158,7 +233,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 
     __syncthreads();  // previous segment is done with q_s / qfrag / merge area
     const int first = t_lo + warp;
-    // ---- unit setup: q rows, max |q * s|, then the Q' hi/lo B-fragments
+    // ---- unit setup: q rows, max |q * s|, then the Q' hi/lo A-fragments
     if (tid == 0) s_misc[0] = 0;
     for (int i = tid; i < G * 128; i += blockDim.x) q_s[i] = load_q(q, q_dtype, unit * G * 128 + i);
     __syncthreads();
@@ -178,43 +253,36 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     const int e_sc = (qmax > 0.0f && qmax < INFINITY)
                          ? max(-90, min(90, 14 - (static_cast<int>((__float_as_uint(qmax) >> 23) & 0xff) - 127)))
                          : 0;
-    for (int i = tid; i < 8 * 32; i += blockDim.x) {
-      const int ks = i >> 5, ln = i & 31, n = ln >> 2, t = ln & 3;
-      uint32_t w[4];
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        const int j = 8 * ks + t + 4 * hh;
+    // A-fragment rows: g < 8 -> Q'_hi of query g, 8 + g -> Q'_lo of query g (zero for g >= G)
+    for (int i = tid; i < 16 * 32; i += blockDim.x) {
+      const int ks = i >> 5, ln = i & 31, g = ln >> 2, t = ln & 3;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (g < G) {
+        const int j = 16 * t + dq_pair<kFused>(ks);
         const float sj = half_bits_to_f32(c.scales[unit * 64 + j]);
         const int ex = c.layout == PQB_HALF_SPLIT ? j : 2 * j;
         const int ey = c.layout == PQB_HALF_SPLIT ? j + 64 : 2 * j + 1;
-        const int g = G == 8 ? n : (n & 3);
         const float vx = ldexpf(q_s[g * 128 + ex] * sj, e_sc), vy = ldexpf(q_s[g * 128 + ey] * sj, e_sc);
         const __half hx = __float2half_rn(vx), hy = __float2half_rn(vy);
         const __half lx = __float2half_rn(vx - __half2float(hx)), ly = __float2half_rn(vy - __half2float(hy));
-        if constexpr (G == 8) {
-          w[hh] = h2_bits(__halves2half2(hx, hy));
-          w[2 + hh] = h2_bits(__halves2half2(lx, ly));
-        } else {  // columns 0-3: Q_hi, 4-7: Q_lo
-          w[hh] = n < 4 ? h2_bits(__halves2half2(hx, hy)) : h2_bits(__halves2half2(lx, ly));
-          w[2 + hh] = 0u;
-        }
+        const uint32_t hb = h2_bits(__halves2half2(hx, hy)), lb = h2_bits(__halves2half2(lx, ly));
+        v = make_uint4(hb, lb, hb, lb);  // a2 / a3 (k + 8) repeat a0 / a1: they multiply K_lo
       }
-      qfrag[i] = make_uint4(w[0], w[1], w[2], w[3]);
+      qfrag[i] = v;
     }
     __syncthreads();
-    uint32_t bq[8][4];
+    uint32_t aq[16][4];
 #pragma unroll
-    for (int ks = 0; ks < 8; ++ks) {
+    for (int ks = 0; ks < 16; ++ks) {
       const uint4 v = qfrag[ks * 32 + lane];
-      bq[ks][0] = v.x;
-      bq[ks][1] = v.y;
-      bq[ks][2] = v.z;
-      bq[ks][3] = v.w;
+      aq[ks][0] = v.x;
+      aq[ks][1] = v.y;
+      aq[ks][2] = v.z;
+      aq[ks][3] = v.w;
     }
     const float xscale = ldexpf(sm_scale_log2, -e_sc);
 
-    // ---- lane 0 fills this warp's ring with its first tiles (after the setup:
-    // measured faster than overlapping it, scripts/ab_probe.sh)
+    // ---- lane 0 fills this warp's ring with its first tiles
     if (lane == 0) {
 #pragma unroll
       for (int s = 0; s < kStages; ++s) {
@@ -222,12 +290,13 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         if (tile < t_hi) {
           fence_proxy_async_smem();
           const uint32_t sl = (k_iter + s) % kStages;
-          issue_tile<M, N>(my_area + sl * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, tile / tpp), tile,
-                           tpp, true, bar + sl);
+          issue_tile<M, N>(my_area + sl * Cfg::kStageBytes, c.store,
+                           page_base_c(c.store, unit, PROBE == 2 ? 0 : tile / tpp), PROBE == 2 ? 0 : tile, tpp, true,
+                           bar + sl);
         }
       }
     }
-    float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.0f, 0.0f};
+    float m_run = -INFINITY, l_run = 0.0f;  // query g8 (lanes g8 < G)
     float d[8][4];
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt)
@@ -240,85 +309,46 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       mbar_wait(bar + s, (k_iter / kStages) & 1);
       const uint8_t* st = my_area + s * Cfg::kStageBytes;
       const int tok0 = tile * kTile;
-
-      // ---- S^T = K^ . Q'^T on the tensor cores, two 16-token m-tiles
-      float sc[2][4], sc2[2][4];  // two MMA accumulation chains per m-tile, summed after
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt) {
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sc[mt][k] = sc2[mt][k] = 0.0f;
-        uint32_t wa[2][2 * M + 1], wr[2][2 * N + 1];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = 16 * mt + g8 + 8 * h;
-          const uint32_t* ra = reinterpret_cast<const uint32_t*>(st + r * 8 * M);
-          const uint32_t* rr = reinterpret_cast<const uint32_t*>(st + Cfg::kABytes + r * 8 * N);
-          if constexpr (M % 2 == 0) {
-#pragma unroll
-            for (int k = 0; k < 2 * M; k += 4) {
-              const uint4 v = *reinterpret_cast<const uint4*>(ra + k);
-              wa[h][k] = v.x; wa[h][k + 1] = v.y; wa[h][k + 2] = v.z; wa[h][k + 3] = v.w;
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 2 * M; k += 2) {
-              const uint2 v = *reinterpret_cast<const uint2*>(ra + k);
-              wa[h][k] = v.x; wa[h][k + 1] = v.y;
-            }
-          }
-          if constexpr (N % 2 == 0) {
-#pragma unroll
-            for (int k = 0; k < 2 * N; k += 4) {
-              const uint4 v = *reinterpret_cast<const uint4*>(rr + k);
-              wr[h][k] = v.x; wr[h][k + 1] = v.y; wr[h][k + 2] = v.z; wr[h][k + 3] = v.w;
-            }
-          } else {
-#pragma unroll
-            for (int k = 0; k < 2 * N; k += 2) {
-              const uint2 v = *reinterpret_cast<const uint2*>(rr + k);
-              wr[h][k] = v.x; wr[h][k + 1] = v.y;
-            }
-          }
-          wa[h][2 * M] = 0u;
-          wr[h][2 * N] = 0u;
-          const bool live = tok0 + r < Tq;  // residual / past-the-end rows: radius 0 => key 0
-          // pre-shift so code (4i + t4) sits at bit 4iB
-#pragma unroll
-          for (int k = 0; k < 2 * M; ++k) wa[h][k] = __funnelshift_r(wa[h][k], wa[h][k + 1], t4 * M);
-#pragma unroll
-          for (int k = 0; k < 2 * N; ++k) wr[h][k] = live ? __funnelshift_r(wr[h][k], wr[h][k + 1], t4 * N) : 0u;
+      if constexpr (PROBE == 1) {
+        __syncwarp();
+        if (lane == 0 && nt < t_hi) {
+          fence_proxy_async_smem();
+          issue_tile<M, N>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, nt / tpp), nt, tpp,
+                           true, bar + s);
         }
-#pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          uint32_t ahi[4], alo[4];
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            // pairs i = 2ks (a0 / a1: k 2t4..) and 2ks + 1 (a2 / a3: k 2t4 + 8..)
-            uint32_t e0, e1;
-            dq_index2<M, N>(wa[h], wr[h], 2 * ks, e0, e1);
-            const uint2 t0 = *reinterpret_cast<const uint2*>(ptab_l + (e0 << 7));
-            const uint2 t1 = *reinterpret_cast<const uint2*>(ptab_l + (e1 << 7));
-            ahi[h] = t0.x;
-            alo[h] = t0.y;
-            ahi[2 + h] = t1.x;
-            alo[2 + h] = t1.y;
-          }
-          mma_f16(sc[mt], ahi[0], ahi[1], ahi[2], ahi[3], bq[ks][0], bq[ks][1]);
-          mma_f16(sc2[mt], alo[0], alo[1], alo[2], alo[3], bq[ks][0], bq[ks][1]);
-          if constexpr (G == 8) mma_f16(sc2[mt], ahi[0], ahi[1], ahi[2], ahi[3], bq[ks][2], bq[ks][3]);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k) sc[mt][k] += sc2[mt][k];
+        continue;
       }
-      if constexpr (G == 4) {  // fold columns q (hi) and q + 4 (lo): lanes t4 and t4 ^ 2
+
+      // ---- S = Q' . K^T on the tensor cores: n-block nb = tokens 8 nb .. 8 nb + 7;
+      // this lane gathers the keys of token 8 nb + g8 (B column g8).
+      float sc[4][4];
+      {
+        DqIdx<M, N> ix[4];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int nb = 0; nb < 4; ++nb) {
+          const int r = 8 * nb + g8;
+          ix[nb].load(st + r * 8 * M, st + Cfg::kABytes + r * 8 * N, t4, tok0 + r < Tq);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) sc[mt][k] += __shfl_xor_sync(0xffffffffu, sc[mt][k], 2);
+          for (int k = 0; k < 4; ++k) sc[nb][k] = 0.0f;
+        }
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks) {
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) {
+            const uint2 t = lds_u2(ix[nb].addr(ptab_l, ks));
+            mma_f16(sc[nb], aq[ks][0], aq[ks][1], aq[ks][2], aq[ks][3], t.x, t.y);
+          }
+        }
+      }
+      // lane (g8, t4): query g8, tokens 8 nb + 2 t4 + j  (hi row + lo row)
+      float x[4][2];
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb) {
+        x[nb][0] = sc[nb][0] + sc[nb][2];
+        x[nb][1] = sc[nb][1] + sc[nb][3];
       }
       // ---- residual window (fp32 keys): exact dots, lane = token (rare tiles)
       if (tok0 + kTile > Tq && Tq < T) {
-        float* rbuf = reinterpret_cast<float*>(pbuf);  // [32][8], scaled like C
         const int tok = tok0 + lane;
         float acc[G];
 #pragma unroll
@@ -335,74 +365,61 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         for (int g = 0; g < 8; ++g) rbuf[lane * 8 + g] = g < G ? ldexpf(acc[g], e_sc) : 0.0f;
         __syncwarp();
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+        for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const int r = 16 * mt + g8 + 8 * (k >> 1), col = 2 * t4 + (k & 1);
-            if (tok0 + r >= Tq && col < G) sc[mt][k] += rbuf[r * 8 + col];
+          for (int j = 0; j < 2; ++j) {
+            const int r = 8 * nb + 2 * t4 + j;
+            if (tok0 + r >= Tq) x[nb][j] += rbuf[r * 8 + g8];
           }
         __syncwarp();
       }
-      // ---- online softmax: lane holds queries 2t4, 2t4+1 for tokens {g8, g8+8} + 16mt
-      float alpha[2];
-      bool rescale = false;
+      // ---- online softmax (query g8; the four t4 lanes share it)
+      float mx = -INFINITY;
 #pragma unroll
-      for (int cq = 0; cq < 2; ++cq) {
-        float x[4];
-        float mx = -INFINITY;
+      for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const int mt = v >> 1, h = v & 1;
-          const int r = 16 * mt + g8 + 8 * h;
-          x[v] = tok0 + r < T ? sc[mt][2 * h + cq] * xscale : -INFINITY;
-          mx = fmaxf(mx, x[v]);
+        for (int j = 0; j < 2; ++j) {
+          x[nb][j] = tok0 + 8 * nb + 2 * t4 + j < T ? x[nb][j] * xscale : -INFINITY;
+          mx = fmaxf(mx, x[nb][j]);
         }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-        const float mn = fmaxf(m_run[cq], mx);
-        alpha[cq] = exp2f(m_run[cq] - mn);
-        rescale |= mn != m_run[cq];
-        m_run[cq] = mn;
-        float ls = 0.0f;
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float mn = fmaxf(m_run, mx);
+      const float alpha = fast_exp2(m_run - mn);
+      const bool rescale = mn != m_run;
+      m_run = mn;
+      float ls = 0.0f;
+      uint32_t phi[4], plo[4];  // bf16x2 (tokens 8 nb + 2 t4, +1)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const float p = exp2f(x[v] - mn);
-          ls += p;
-          sc[v >> 1][2 * (v & 1) + cq] = p;
-        }
-        l_run[cq] = fmaf(l_run[cq], alpha[cq], ls);
-      }
-      // P -> pbuf [hi/lo][token][8 queries] bf16 (queries >= G stay zero)
-      const bool qvalid = 2 * t4 < G;
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int mt = v >> 1, h = v & 1;
-        const int r = 16 * mt + g8 + 8 * h;
-        const float p0 = qvalid ? sc[mt][2 * h] : 0.0f, p1 = qvalid ? sc[mt][2 * h + 1] : 0.0f;
+      for (int nb = 0; nb < 4; ++nb) {
+        const float p0 = fast_exp2(x[nb][0] - mn), p1 = fast_exp2(x[nb][1] - mn);
+        ls += p0 + p1;
         const __nv_bfloat162 hi = __floats2bfloat162_rn(p0, p1);
         const float2 hf = __bfloat1622float2(hi);
         const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
-        *reinterpret_cast<__nv_bfloat162*>(pbuf + r * 16 + 4 * t4) = hi;
-        *reinterpret_cast<__nv_bfloat162*>(pbuf + kTile * 16 + r * 16 + 4 * t4) = lo;
+        phi[nb] = *reinterpret_cast<const uint32_t*>(&hi);
+        plo[nb] = *reinterpret_cast<const uint32_t*>(&lo);
       }
-      if (__any_sync(0xffffffffu, rescale)) {
+      l_run = fmaf(l_run, alpha, ls);
+      if (__any_sync(0xffffffffu, rescale && g8 < G)) {
+        const float a0 = __shfl_sync(0xffffffffu, alpha, qc0 * 4), a1 = __shfl_sync(0xffffffffu, alpha, qc1 * 4);
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
-          d[mt][0] *= alpha[0];
-          d[mt][1] *= alpha[1];
-          d[mt][2] *= alpha[0];
-          d[mt][3] *= alpha[1];
+          d[mt][0] *= a0;
+          d[mt][1] *= a1;
+          d[mt][2] *= a0;
+          d[mt][3] *= a1;
         }
       }
-      __syncwarp();
-      // ---- P.V on tensor cores (as decode_fast_kernel): P^T fragments via ldmatrix.trans
-      uint32_t b[2][2][2];  // [pl][ks][reg]
-      {
-        const uint32_t pb0 = smem_u32(pbuf) + lane * 16;
-        ldsm_x4_trans(pb0, b[0][0][0], b[0][0][1], b[0][1][0], b[0][1][1]);
-        ldsm_x4_trans(pb0 + kTile * 16, b[1][0][0], b[1][0][1], b[1][1][0], b[1][1][1]);
+      if constexpr (kPacked) {  // columns 4..7 (lanes 16..31) take P_lo of query g8 - 4
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+          const uint32_t o = __shfl_xor_sync(0xffffffffu, plo[nb], 16);
+          phi[nb] = lane < 16 ? phi[nb] : o;
+        }
       }
+      // ---- P.V on tensor cores: O^T[128 x 8] += V^T[128 x 32] . P^T[32 x 8];
+      // the P^T B-fragments are the score registers (k-step ks = n-blocks 2ks, 2ks+1)
       const uint32_t vbase = smem_u32(st + Cfg::kABytes + Cfg::kRBytes) + ld_row;
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
@@ -410,46 +427,45 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         for (int ks = 0; ks < 2; ++ks) {
           uint32_t a0, a1, a2, a3;
           ldsm_x4_trans(vbase + ks * 16 * 256 + (ld_chunk ^ (mt << 5)), a0, a1, a2, a3);
-          mma_bf16(d[mt], a0, a1, a2, a3, b[0][ks][0], b[0][ks][1]);
-          mma_bf16(d[mt], a0, a1, a2, a3, b[1][ks][0], b[1][ks][1]);
+          mma_bf16(d[mt], a0, a1, a2, a3, phi[2 * ks], phi[2 * ks + 1]);
+          if constexpr (!kPacked) mma_bf16(d[mt], a0, a1, a2, a3, plo[2 * ks], plo[2 * ks + 1]);
         }
       }
       __syncwarp();
       if (lane == 0 && nt < t_hi) {
         fence_proxy_async_smem();
-        issue_tile<M, N>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, nt / tpp), nt, tpp,
-                         true, bar + s);
+        issue_tile<M, N>(my_area + s * Cfg::kStageBytes, c.store,
+                         page_base_c(c.store, unit, PROBE == 2 ? 0 : nt / tpp), PROBE == 2 ? 0 : nt, tpp, true,
+                         bar + s);
       }
     }
 
     // ---- segment epilogue: per-warp (m, l, o) -> shared, then the common merge
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+    l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+    if constexpr (kPacked) {  // O = columns q (P_hi) + q + 4 (P_lo): lanes t4, t4 ^ 2
 #pragma unroll
-    for (int cq = 0; cq < 2; ++cq) {
-      l_run[cq] += __shfl_xor_sync(0xffffffffu, l_run[cq], 4);
-      l_run[cq] += __shfl_xor_sync(0xffffffffu, l_run[cq], 8);
-      l_run[cq] += __shfl_xor_sync(0xffffffffu, l_run[cq], 16);
+      for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d[mt][k] += __shfl_xor_sync(0xffffffffu, d[mt][k], 2);
     }
     __syncthreads();
     float* red = reinterpret_cast<float*>(warp_area);
     float* mine = red + warp * G * 132;
-    if (g8 == 0) {
-#pragma unroll
-      for (int cq = 0; cq < 2; ++cq) {
-        const int qq = 2 * t4 + cq;
-        if (qq < G) {
-          mine[qq * 132] = m_run[cq];
-          mine[qq * 132 + 1] = l_run[cq];
-        }
-      }
+    if (t4 == 0 && g8 < G) {
+      mine[g8 * 132] = m_run;
+      mine[g8 * 132 + 1] = l_run;
     }
+    if (qc0 < G && (!kPacked || t4 < 2)) {
 #pragma unroll
-    for (int mt = 0; mt < 8; ++mt) {
-      const int dim = 16 * mt + g8;
-      if (2 * t4 < G) {
-        mine[(2 * t4) * 132 + 4 + dim] = d[mt][0];
-        mine[(2 * t4) * 132 + 4 + dim + 8] = d[mt][2];
-        mine[(2 * t4 + 1) * 132 + 4 + dim] = d[mt][1];
-        mine[(2 * t4 + 1) * 132 + 4 + dim + 8] = d[mt][3];
+      for (int mt = 0; mt < 8; ++mt) {
+        const int dim = 16 * mt + g8;
+        mine[qc0 * 132 + 4 + dim] = d[mt][0];
+        mine[qc0 * 132 + 4 + dim + 8] = d[mt][2];
+        if (qc1 < G) {
+          mine[qc1 * 132 + 4 + dim] = d[mt][1];
+          mine[qc1 * 132 + 4 + dim + 8] = d[mt][3];
+        }
       }
     }
     finish_segment<G>(ep, ws, unit, red, s_misc + 1, tid, blockDim.x);
@@ -458,19 +474,20 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 
 // ------------------------------------------------------------------ host side
 
-template <int G, int M, int N>
+template <int G, int M, int N, int PROBE = 0>
 static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s) {
   using Cfg = DqCfg<G, M, N>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(decode_dq_kernel<G, M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) !=
-        cudaSuccess) {
+    if (cudaFuncSetAttribute(decode_dq_kernel<G, M, N, PROBE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             Cfg::kSmem) != cudaSuccess) {
       set_error("cudaFuncSetAttribute(smem=%d) failed", Cfg::kSmem);
       return PQB_ECUDA;
     }
     attr_set = true;
   }
-  decode_dq_kernel<G, M, N><<<grid, kNW * 32, Cfg::kSmem, s>>>(*a.cache, a.q, a.q_dtype, a.sm_scale * kLog2e, ep, ws);
+  decode_dq_kernel<G, M, N, PROBE>
+      <<<grid, kNW * 32, Cfg::kSmem, s>>>(*a.cache, a.q, a.q_dtype, a.sm_scale * kLog2e, ep, ws);
   return PQB_OK;
 }
 
@@ -478,7 +495,10 @@ template <int G>
 static int dispatch_dq_mn(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s,
                           bool& handled) {
   handled = true;
-  switch (a.cache->angle_bits * 10 + a.cache->radius_bits) {
+  const int mn = a.cache->angle_bits * 10 + a.cache->radius_bits;
+  if (mn == 44 && (a.flags & PQB_DECODE_PROBE_MEM)) return launch_dq<G, 4, 4, 1>(a, ep, ws, grid, s);
+  if (mn == 44 && (a.flags & PQB_DECODE_PROBE_COMPUTE)) return launch_dq<G, 4, 4, 2>(a, ep, ws, grid, s);
+  switch (mn) {
     case 44: return launch_dq<G, 4, 4>(a, ep, ws, grid, s);
     case 32: return launch_dq<G, 3, 2>(a, ep, ws, grid, s);
     case 22: return launch_dq<G, 2, 2>(a, ep, ws, grid, s);
