@@ -24,7 +24,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "pqb200"
 LIB = PKG / "libpqb200.so"
-SOURCES = ["encode.cu", "decode.cu", "decode_dq.cu", "misc.cu", "abi.cu"]
+SOURCES = ["encode.cu", "encode_fast.cu", "decode.cu", "decode_dq.cu", "misc.cu", "abi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3",

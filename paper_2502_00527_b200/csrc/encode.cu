@@ -17,6 +17,9 @@
 #include "polar_math.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+#include <cstring>
+
 #include <algorithm>
 
 namespace pqb {
@@ -787,6 +790,9 @@ static void dispatch_m(const EncodeArgs& a, int64_t chunk, dim3 grid, cudaStream
 int launch_encode(const EncodeArgs& a, cudaStream_t s) {
   const int half = a.d / 2;
   if (a.tokens == 0) return 0;
+  // PQB_ENCODE_KERNEL=v8 forces the per-call-grid kernel below (A/B and parity tests)
+  const char* kern = std::getenv("PQB_ENCODE_KERNEL");
+  if (!(kern && std::strcmp(kern, "v8") == 0) && launch_encode_fast(a, s)) return 0;
   if (a.vector_ok) {
     const int64_t chunk = 2048;
     dim3 grid(static_cast<unsigned>((a.tokens + chunk - 1) / chunk), static_cast<unsigned>(a.n_units));

@@ -1,0 +1,441 @@
+// HP-1 K2, persistent TMA-fed encoder for the common shapes (sm_100a):
+// encode_fast_kernel<DT, LAYOUT, M, N>.
+//
+//   reference  quantize_subvectors (polar_codec.py:281-302), pack_stream (:98-110),
+//              PackedKVCache._encode_block (kv_cache.py:191-197)
+//
+// Same arithmetic contract as encode_v8 (polar_math.cuh): a fast fp32 decision
+// per sub-vector pair, and the exact double-precision pipeline for a thread's
+// eight pairs whenever one of them lies within the ambiguity band of an angle
+// edge or a radius rounding boundary.  What changes is the cost per pair
+// (encode_v8 measured 78 instructions per pair, ALU-pipe bound,
+// profiles/r01/ncu_encode_fast.json):
+//   * m, n are compile-time: codes pack into 32-bit words with constant shifts;
+//     for m = 4 / n = 4 a thread's eight codes are exactly one stream word.
+//   * the octant fold works on s = |x| + |y| and a = ||x| - |y||:
+//       sign(mn - mx tan b) = sign(s - a (1 + tan b) / (1 - tan b)),
+//     one FFMA per edge with an immediate; the ambiguity test of all pairs and
+//     edges folds into one running maximum.
+//   * the radius code is taken from the float bits (magic-number add) and
+//     packed with IMADs; clamp events are counted with saturating adds.
+//   * keys arrive through per-warp rings of TMA bulk copies (4 KB stages), the
+//     grid is persistent (one 16-warp CTA per SM) and warps take 512-token
+//     (unit, chunk) items round-robin; no CTA-wide barrier in the loop, so the
+//     rare exact-path lane stalls only its own warp.
+// Requirements (checked by the launcher, else encode_v8): d = 128, dense
+// 16-byte aligned rows, page_tokens % 16 == 0, start token % 16 == 0,
+// m in {2, 3, 4}, n in {2, 3, 4}.
+#include "kernels.h"
+#include "polar_math.cuh"
+
+#include <algorithm>
+
+namespace pqb {
+
+namespace {
+
+constexpr int kEfWarps = 16;     // warps per CTA (one CTA per SM)
+constexpr int kEfStages = 3;     // ring depth per warp
+constexpr int kEfItemTok = 512;  // tokens per work item (one unit)
+constexpr int kEfAlign = 16;     // start token / page alignment the kernel needs
+
+template <int DT>
+struct EfCfg {
+  static constexpr int kRowBytes = 128 * DType<DT>::kBytes;
+  static constexpr int kStageBytes = 4096;                  // per-warp stage
+  static constexpr int kStageTok = kStageBytes / kRowBytes;  // 16 (2-byte keys) or 8 (fp32)
+  static constexpr int kSmem = kEfWarps * kEfStages * kStageBytes;
+};
+
+// Octant-fold constants of angle_bits M (M >= 3): edge i at b_i, t = tan(b_i):
+//   K_i = (1 + t) / (1 - t),  e_i = s - a K_i  (sign of mn - mx t),
+//   band: |mn - mx t| <= thr_i (mx + mn)  <=>  |e_i| <= 2 thr_i / (1 - t) s.
+// The band constant is inflated by 1% (covers the fp32 rounding of s, a, K_i
+// and the FFMA, <= 1e-6 s; polar_math.cuh has the pipeline's error budget).
+__host__ __device__ constexpr float ef_k(int m, int i) { return (1.0f + edge_tan(m, i)) / (1.0f - edge_tan(m, i)); }
+__host__ __device__ constexpr float ef_band(int m, int i) { return 2.02f * edge_thr(m, i) / (1.0f - edge_tan(m, i)); }
+template <int M>
+__host__ __device__ constexpr float ef_band_max() {
+  float b = 0.0f;
+  for (int i = 0; i < (1 << (M - 3)); ++i) b = ef_band(M, i) > b ? ef_band(M, i) : b;
+  return b;
+}
+
+// Exact |x| == |y| at m = 2 (frequent with bf16 keys): atan2f is fl32(+-pi/4)
+// or fl32(+-3pi/4); the reference pipeline's code for each sign pattern.
+PQB_DEV uint32_t ef_m2_diag(float x, float y) {
+  const uint32_t sx = __float_as_uint(x) >> 31;
+  return angle_code_from_phi(copysignf(sx ? 2.35619449615478515625f : 0.785398185253143310546875f, y), 2);
+}
+
+// Fast codes of one pair.  Returns the angle code (before the canonical
+// origin rule) and the rounded radius ratio rq; `worst` collects the
+// ambiguity metric (>= 0: inside a band), `rok` the magnitude-range check.
+template <int M>
+PQB_DEV uint32_t ef_angle(float x, float y, float& worst) {
+  const float ax = fabsf(x), ay = fabsf(y);
+  const float s = ax + ay, dif = ax - ay, a = fabsf(dif);
+  const uint32_t sx = __float_as_uint(x) >> 31, sy = __float_as_uint(y) >> 31;
+  constexpr int Q = 1 << (M - 2), H = 2 * Q;
+  int k0;
+  if constexpr (M == 2) {
+    // the only edge is the diagonal: k0 = 1 iff |y| > |x|.  An exact tie
+    // |x| == |y| (frequent with bf16 keys) is decided by ef_m2_diag, not banded.
+    if (a == 0.0f) return ef_m2_diag(x, y);
+    worst = fmaxf(worst, fmaf(kQuadEdgeThr * 1.01f, s, -a));
+    k0 = dif < 0.0f ? 1 : 0;
+  } else {
+    constexpr int NB = 1 << (M - 3);
+    int kk = 0;
+    float mn_e = INFINITY;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const float e = fmaf(-a, ef_k(M, i), s);
+      kk += e > 0.0f ? 1 : 0;
+      mn_e = fminf(mn_e, fabsf(e));
+    }
+    worst = fmaxf(worst, fmaf(ef_band_max<M>(), s, -mn_e));
+    k0 = dif < 0.0f ? Q - kk : kk;
+  }
+  const int base = sx ? (sy ? 0 : 2 * H) : H;
+  const int c = (sx ^ sy) ? base - k0 : base + k0;
+  return static_cast<uint32_t>(c) & (2u * H - 1u);
+}
+
+PQB_DEV float ef_radius(float x, float y, float inv, float& worst, bool& rok) {
+  const float r2 = fmaf(x, x, y * y);
+  rok &= in_safe_range_nonneg(r2);
+  const float q = r2 * rsqrt_approx(r2) * inv;
+  const float rq = rintf(q);
+  // |q - rq| >= 0.5 - 2^-18 q  <=>  band
+  worst = fmaxf(worst, fmaf(q, 0x1p-18f, fabsf(q - rq)) - 0.5f);
+  return rq;
+}
+
+// Word w (0 <= w < 2B) of a token row of B-bit codes when lane-in-row j holds
+// codes 8j .. 8j+7 as chunk c (8B bits).  Shuffles stay inside the row's 8 lanes.
+template <int B>
+PQB_DEV uint32_t ef_row_word(uint32_t c, int j) {
+  if constexpr (B == 4) {
+    return c;
+  } else if constexpr (B == 2) {
+    const uint32_t hi = __shfl_sync(0xffffffffu, c, 2 * j + 1, 8);
+    const uint32_t lo = __shfl_sync(0xffffffffu, c, 2 * j, 8);
+    return lo | (hi << 16);
+  } else {  // B == 3: 24-bit chunks; word j spans chunks a, a + 1
+    const int bit = 32 * j, a = bit / 24, o = bit - 24 * a;
+    const uint32_t c0 = __shfl_sync(0xffffffffu, c, a & 7, 8);
+    const uint32_t c1 = __shfl_sync(0xffffffffu, c, (a + 1) & 7, 8);
+    return (c0 >> o) | (c1 << (24 - o));
+  }
+}
+
+struct EfArgs {
+  const void* keys;
+  int64_t T;
+  int64_t unit_stride;  // elements
+  int64_t n_units;
+  int64_t items, chunks_per_unit;
+  const uint16_t* scales;
+  pqb_store st;
+  int64_t tok0;  // absolute position of call-token 0 (multiple of 16)
+  unsigned long long* clamp_counts;
+  int32_t* flags;
+};
+
+// Eight codes of B bits per lane of a token row -> the 32-bit chunk, with the
+// canonical forms applied.  Shared by the fast and the exact path.
+template <int M, int N>
+PQB_DEV void ef_pack(const uint32_t (&ac)[8], const float (&rq)[8], uint32_t keep_a, uint32_t keep_r,
+                     float& clamps, uint32_t& ca, uint32_t& cr) {
+  constexpr float kTop = static_cast<float>((1 << N) - 1);
+  constexpr uint32_t kMagic = 0x4B400000u;  // bits of 1.5 * 2^23: f + 1.5*2^23 carries int(f) in the low bits
+  // sum over the 8 fields of kMagic << (N * i), mod 2^32 (removed after packing)
+  constexpr uint32_t kMagicSum = [] {
+    uint32_t t = 0;
+    for (int i = 0; i < 8; ++i) t += kMagic << (N * i);
+    return t;
+  }();
+  ca = 0u;
+  cr = 0u;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    clamps += __saturatef(rq[i] - kTop);  // 1 iff rq >= top + 1 (integers)
+    const float rc = fminf(rq[i], kTop);
+    cr += __float_as_uint(rc + 12582912.0f) << (N * i);
+    const uint32_t a = rc == 0.0f ? (1u << (M - 1)) : ac[i];  // polar_codec.py:297
+    ca += a << (M * i);
+  }
+  cr -= kMagicSum;
+  ca &= keep_a;  // zero-scale channels: both codes 0 (polar_codec.py:298-301)
+  cr &= keep_r;
+}
+
+// Warp-level persistent kernel.  Warp gw (of W = grid * kEfWarps) encodes items
+// gw, gw + W, ...; an item is kEfItemTok consecutive tokens of one unit, read as
+// stages of kEfStageTok tokens through the warp's own ring of TMA bulk copies
+// (lane 0 produces; no CTA-wide barrier, so a lane on the exact path delays
+// only its own warp).  Lane = (row r = lane / 8 of the 4 rows an iteration
+// covers, channel group cg = lane % 8).
+template <int DT, int LAYOUT, int M, int N>
+__global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfArgs p) {
+  using Cfg = EfCfg<DT>;
+  constexpr int kStageTok = Cfg::kStageTok;
+  constexpr int kStagesPerItem = kEfItemTok / kStageTok;
+  extern __shared__ __align__(128) uint8_t esm[];
+  __shared__ uint64_t bars_all[kEfWarps][kEfStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = lane >> 3, cg = lane & 7;
+  uint64_t* bars = bars_all[warp];
+  uint8_t* ring = esm + warp * (kEfStages * Cfg::kStageBytes);
+  const int64_t W = static_cast<int64_t>(gridDim.x) * kEfWarps;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * kEfWarps + warp;
+  const int64_t my_items = p.items > gw ? (p.items - gw + W - 1) / W : 0;
+  const int64_t n_stage = my_items * kStagesPerItem;
+  if (lane == 0) {
+    for (int s = 0; s < kEfStages; ++s) mbar_init(bars + s, 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  // Stage g of this warp = stage g % S of item gw + (g / S) * W; stages past the
+  // unit's end are empty.  Incremental cursors: one 64-bit division per item.
+  struct Cursor {
+    int64_t item, unit, t_item;
+    int st;
+  };
+  auto cursor_item = [&](Cursor& c) {
+    c.unit = c.item / p.chunks_per_unit;
+    c.t_item = (c.item - c.unit * p.chunks_per_unit) * kEfItemTok;
+  };
+  auto cursor_next = [&](Cursor& c) {
+    if (++c.st == kStagesPerItem) {
+      c.st = 0;
+      c.item += W;
+      cursor_item(c);
+    }
+  };
+  auto stage_rows = [&](const Cursor& c) {
+    const int64_t left = p.T - (c.t_item + c.st * kStageTok);
+    return left <= 0 ? 0 : (left < kStageTok ? static_cast<int>(left) : kStageTok);
+  };
+  Cursor pc{gw, 0, 0, 0};  // producer (lane 0)
+  cursor_item(pc);
+  int64_t p_g = 0;
+  auto issue_next = [&]() {
+    const int slot = static_cast<int>(p_g % kEfStages);
+    const int rows = stage_rows(pc);
+    if (rows == 0) {
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bars + slot)) : "memory");
+    } else {
+      const uint32_t bytes = static_cast<uint32_t>(rows) * Cfg::kRowBytes;
+      mbar_arrive_expect_tx(bars + slot, bytes);
+      const uint8_t* src = static_cast<const uint8_t*>(p.keys) +
+                           (pc.unit * p.unit_stride + (pc.t_item + pc.st * kStageTok) * 128) *
+                               static_cast<int64_t>(DType<DT>::kBytes);
+      bulk_g2s(ring + slot * Cfg::kStageBytes, src, bytes, bars + slot);
+    }
+    ++p_g;
+    cursor_next(pc);
+  };
+  if (lane == 0)
+    for (int64_t g = 0; g < kEfStages && g < n_stage; ++g) issue_next();
+
+  int64_t cur_unit = -1;
+  float s32[8], inv[8];
+  uint32_t keep_a = 0u, keep_r = 0u;  // fields of channels with a non-zero scale
+  float clamps = 0.0f;
+  bool bad = false;
+  auto flush_clamps = [&]() {
+    if (cur_unit >= 0 && p.clamp_counts) {
+      unsigned int c = static_cast<unsigned int>(clamps);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0 && c) atomicAdd(p.clamp_counts + cur_unit, static_cast<unsigned long long>(c));
+    }
+    clamps = 0.0f;
+  };
+
+  Cursor cc{gw, 0, 0, 0};  // consumer
+  cursor_item(cc);
+  int64_t pg = 0;  // page of the stage's first token, and its row in the page
+  int in_pg0 = 0;
+  for (int64_t g = 0; g < n_stage; ++g, cursor_next(cc)) {
+    const int64_t unit = cc.unit, t0 = cc.t_item + cc.st * kStageTok;
+    const int rows = stage_rows(cc);
+    if (cc.st == 0) {
+      const int64_t tok = p.tok0 + t0;
+      pg = tok / p.st.page_tokens;
+      in_pg0 = static_cast<int>(tok - pg * p.st.page_tokens);
+    } else {
+      in_pg0 += kStageTok;
+      if (in_pg0 == p.st.page_tokens) {
+        in_pg0 = 0;
+        ++pg;
+      }
+    }
+    if (unit != cur_unit) {  // warp-uniform: flush the clamp count, load this unit's scales
+      flush_clamps();
+      cur_unit = unit;
+      const uint4 sv = __ldg(reinterpret_cast<const uint4*>(p.scales + unit * 64 + 8 * cg));
+      const uint32_t w[4] = {sv.x, sv.y, sv.z, sv.w};
+      keep_a = keep_r = 0u;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        s32[2 * i] = half_bits_to_f32(static_cast<uint16_t>(w[i] & 0xffffu));
+        s32[2 * i + 1] = half_bits_to_f32(static_cast<uint16_t>(w[i] >> 16));
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        inv[i] = s32[i] > 0.0f ? __frcp_rn(s32[i]) : 0.0f;
+        if (s32[i] > 0.0f) {
+          keep_a |= ((1u << M) - 1u) << (M * i);
+          keep_r |= ((1u << N) - 1u) << (N * i);
+        }
+      }
+    }
+    const int slot = static_cast<int>(g % kEfStages);
+    mbar_wait(bars + slot, static_cast<uint32_t>((g / kEfStages) & 1));
+    const int64_t pid = p.st.page_table ? static_cast<int64_t>(__ldg(p.st.page_table + unit * p.st.max_pages + pg))
+                                        : unit * p.st.max_pages + pg;
+    uint8_t* pb = p.st.pool + pid * p.st.page_bytes;
+#pragma unroll 1
+    for (int it = 0; it < kStageTok / 4; ++it) {
+      const int row = 4 * it + r;
+      const bool valid = row < rows;
+      uint32_t ca = 0u, cr = 0u;
+      if (valid) {
+        const uint8_t* rp = ring + slot * Cfg::kStageBytes + row * Cfg::kRowBytes;
+        float x[8], y[8];
+        if constexpr (LAYOUT == PQB_HALF_SPLIT) {
+          load8s<DT>(rp, 8 * cg, x);
+          load8s<DT>(rp, 64 + 8 * cg, y);
+        } else {
+          float v0[8], v1[8];
+          load8s<DT>(rp, 16 * cg, v0);
+          load8s<DT>(rp, 16 * cg + 8, v1);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            x[i] = v0[2 * i]; y[i] = v0[2 * i + 1];
+            x[4 + i] = v1[2 * i]; y[4 + i] = v1[2 * i + 1];
+          }
+        }
+        uint32_t ac[8];
+        float rq[8];
+        float worst = -1.0f;
+        bool rok = true;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          rq[i] = ef_radius(x[i], y[i], inv[i], worst, rok);
+          ac[i] = ef_angle<M>(x[i], y[i], worst);
+        }
+        if (!(worst < 0.0f) || !rok) {
+          // rare: the exact pipeline for this lane's eight pairs (zero-scale
+          // channels are masked in ef_pack and need no exact work)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            if (s32[i] > 0.0f) {
+              bad |= !(fabsf(x[i]) <= 3.40282347e38f && fabsf(y[i]) <= 3.40282347e38f);
+              rq[i] = radius_raw_exact(x[i], y[i], s32[i]);
+              ac[i] = angle_code_exact(x[i], y[i], M);
+            }
+          }
+        }
+        ef_pack<M, N>(ac, rq, keep_a, keep_r, clamps, ca, cr);
+      }
+      // ---- the row's 2M angle words and 2N radius words (a stage never
+      // straddles a page).  Row-word shuffles run on all lanes.
+      const uint32_t wa = ef_row_word<M>(ca, cg), wr = ef_row_word<N>(cr, cg);
+      if (valid) {
+        const int in_pg = in_pg0 + row;
+        if (cg < 2 * M) reinterpret_cast<uint32_t*>(pb + p.st.angle_off + in_pg * 8 * M)[cg] = wa;
+        if (cg < 2 * N) reinterpret_cast<uint32_t*>(pb + p.st.radius_off + in_pg * 8 * N)[cg] = wr;
+      }
+    }
+    __syncwarp();  // every lane is done with this slot
+    if (lane == 0 && g + kEfStages < n_stage) {
+      fence_proxy_async_smem();
+      issue_next();
+    }
+  }
+  flush_clamps();
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.flags, PQB_FLAG_NONFINITE);
+}
+
+int ef_num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int DT, int LAYOUT, int M, int N>
+void launch_ef(const EfArgs& p, cudaStream_t s) {
+  using Cfg = EfCfg<DT>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(encode_fast_kernel<DT, LAYOUT, M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg::kSmem);
+    attr = true;
+  }
+  const int64_t grid = std::min<int64_t>((p.items + kEfWarps - 1) / kEfWarps, ef_num_sms());
+  encode_fast_kernel<DT, LAYOUT, M, N><<<static_cast<unsigned>(grid), kEfWarps * 32, Cfg::kSmem, s>>>(p);
+}
+
+template <int DT, int LAYOUT>
+bool dispatch_ef_mn(const EfArgs& p, int m, int n, cudaStream_t s) {
+  switch (m * 10 + n) {
+    case 44: launch_ef<DT, LAYOUT, 4, 4>(p, s); return true;
+    case 42: launch_ef<DT, LAYOUT, 4, 2>(p, s); return true;
+    case 43: launch_ef<DT, LAYOUT, 4, 3>(p, s); return true;
+    case 34: launch_ef<DT, LAYOUT, 3, 4>(p, s); return true;
+    case 32: launch_ef<DT, LAYOUT, 3, 2>(p, s); return true;
+    case 33: launch_ef<DT, LAYOUT, 3, 3>(p, s); return true;
+    case 24: launch_ef<DT, LAYOUT, 2, 4>(p, s); return true;
+    case 22: launch_ef<DT, LAYOUT, 2, 2>(p, s); return true;
+    case 23: launch_ef<DT, LAYOUT, 2, 3>(p, s); return true;
+    default: return false;
+  }
+}
+
+}  // namespace
+
+// The persistent fast encoder when the call qualifies; false -> caller uses encode_v8.
+bool launch_encode_fast(const EncodeArgs& a, cudaStream_t s) {
+  const pqb_store& st = *a.store;
+  const int eb = a.key_dtype == PQB_F32 ? 4 : 2;
+  const bool ok = a.vector_ok && a.d == 128 && a.tok_stride == 128 && a.tok_offset == nullptr &&
+                  a.tok_offset_const % kEfAlign == 0 && st.page_tokens % kEfAlign == 0 &&
+                  reinterpret_cast<uintptr_t>(a.keys) % 16 == 0 && (a.unit_stride * eb) % 16 == 0 &&
+                  reinterpret_cast<uintptr_t>(a.scales) % 16 == 0 && a.angle_bits >= 2 && a.angle_bits <= 4 &&
+                  a.radius_bits >= 2 && a.radius_bits <= 4 && st.angle_off % 4 == 0 && st.radius_off % 4 == 0 &&
+                  st.page_bytes % 4 == 0 && reinterpret_cast<uintptr_t>(st.pool) % 4 == 0;
+  if (!ok || a.tokens == 0 || a.n_units == 0) return false;
+  EfArgs p;
+  p.keys = a.keys;
+  p.T = a.tokens;
+  p.unit_stride = a.unit_stride;
+  p.n_units = a.n_units;
+  p.chunks_per_unit = (a.tokens + kEfItemTok - 1) / kEfItemTok;
+  p.items = a.n_units * p.chunks_per_unit;
+  p.scales = a.scales;
+  p.st = st;
+  p.tok0 = a.tok_offset_const;
+  p.clamp_counts = a.clamp_counts;
+  p.flags = a.flags;
+  const int m = a.angle_bits, n = a.radius_bits;
+  switch (a.key_dtype * 2 + a.layout) {
+    case PQB_F32 * 2 + PQB_ADJACENT: return dispatch_ef_mn<PQB_F32, PQB_ADJACENT>(p, m, n, s);
+    case PQB_F32 * 2 + PQB_HALF_SPLIT: return dispatch_ef_mn<PQB_F32, PQB_HALF_SPLIT>(p, m, n, s);
+    case PQB_BF16 * 2 + PQB_ADJACENT: return dispatch_ef_mn<PQB_BF16, PQB_ADJACENT>(p, m, n, s);
+    case PQB_BF16 * 2 + PQB_HALF_SPLIT: return dispatch_ef_mn<PQB_BF16, PQB_HALF_SPLIT>(p, m, n, s);
+    case PQB_F16 * 2 + PQB_ADJACENT: return dispatch_ef_mn<PQB_F16, PQB_ADJACENT>(p, m, n, s);
+    default: return dispatch_ef_mn<PQB_F16, PQB_HALF_SPLIT>(p, m, n, s);
+  }
+}
+
+}  // namespace pqb

@@ -276,3 +276,101 @@ def test_exact_diagonal_ties(m):
     ea, er, _ = exact.encode(keys, s16, m, 4, 1)
     a, r = (t.cpu().numpy() for t in cache.code_arrays(0))
     assert np.array_equal(a, ea) and np.array_equal(r, er)
+
+
+def _encode_raw(keys: torch.Tensor, s16: np.ndarray, cfg, page_tokens: int, kernel: str):
+    """K2 alone with given scales into a fresh shuffled paged cache; kernel
+    'fast' (encode_fast.cu when the call qualifies) or 'v8' (forced)."""
+    import os
+
+    from paper_2502_00527_b200.codec import encode_device
+
+    U, T, d = keys.shape
+    cache = pq.PolarKVCache(cfg, U, d, 0, capacity=T + 1, page_tokens=page_tokens, shuffle_pages=True)
+    cache.scales16.copy_(torch.from_numpy(s16.view(np.float16)).cuda())
+    old = os.environ.pop("PQB_ENCODE_KERNEL", None)
+    if kernel == "v8":
+        os.environ["PQB_ENCODE_KERNEL"] = "v8"
+    try:
+        encode_device(keys, cache.scales16, cfg, cache.store_ref(), clamp_counts=cache.clamp_counts)
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("PQB_ENCODE_KERNEL", None)
+        if old is not None:
+            os.environ["PQB_ENCODE_KERNEL"] = old
+    cache.host_quant[:] = T
+    return cache
+
+
+def _hard_keys(U: int, T: int, seed: int) -> np.ndarray:
+    """Synthetic keys plus the cases the fast path must route or resolve:
+    bin-edge angles, exact diagonal ties, axis points, zero rows, a dead
+    channel (scale 0), tiny and large magnitudes."""
+    keys = np.stack([po.synthetic_keys(T, 128, seed=seed + u, outliers=(0, 1)) for u in range(U)])
+    rng = np.random.default_rng(seed)
+    # bin edges of every m in {2, 3, 4} (+- a few ulp) on channel pairs 10..13
+    for j, m in zip(range(10, 13), (2, 3, 4)):
+        k = rng.integers(0, 1 << m, size=(U, T))
+        phi = (k + 0.5) * np.pi / (1 << (m - 1)) - np.pi + rng.choice([-2e-7, 0.0, 2e-7], size=(U, T))
+        r = rng.uniform(0.2, 2.0, size=(U, T))
+        keys[:, :, j], keys[:, :, 64 + j] = (r * np.cos(phi)).astype(np.float32), (r * np.sin(phi)).astype(np.float32)
+    v = rng.standard_normal((U, T)).astype(np.float32)
+    keys[:, :, 20], keys[:, :, 84] = v, -v  # |x| == |y|
+    keys[:, ::5, 21] = 0.0  # axis points
+    keys[:, ::13, 33] = 0.0
+    keys[:, ::13, 97] = 0.0  # origin
+    keys[:, :, 7] = 0.0
+    keys[:, :, 71] = 0.0  # dead channel 7 -> scale 0
+    keys[:, ::17, 40] *= 1e-12  # tiny
+    return keys
+
+
+@pytest.mark.parametrize("m,n", [(4, 4), (3, 2), (2, 4), (2, 2), (4, 2), (3, 4), (3, 3), (2, 3), (4, 3)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("layout", [1, 0])
+def test_fast_encoder_vs_v8_and_exact(m, n, dtype, layout):
+    """encode_fast.cu against the per-call-grid kernel and the exact C oracle:
+    codes bit-identical, clamp counts equal (scales shrunk on a few channels so
+    radii clamp), ragged T (partial 1024-token item and 32-token stage)."""
+    U, T = 3, 2 * 1024 + 357
+    keys_np = _hard_keys(U, T, seed=40 + m * 10 + n)
+    keys = torch.from_numpy(keys_np).to(dtype)
+    if layout == 0:  # ADJACENT: interleave the HALF_SPLIT halves
+        keys = torch.stack([keys[..., :64], keys[..., 64:]], dim=-1).reshape(U, T, 128)
+    keys_f = keys.float().numpy()
+    cfg = pq.QuantConfig(m, n, LAY[layout])
+    s16 = np.stack([exact.scales(keys_f[u], n, layout) for u in range(U)])
+    s16 = s16.view(np.float16).copy()
+    s16[:, 30:34] = (s16[:, 30:34].astype(np.float32) * 0.6).astype(np.float16)  # clamps
+    fast = _encode_raw(keys.cuda(), s16.view(np.uint16), cfg, 128, "fast")
+    ref = _encode_raw(keys.cuda(), s16.view(np.uint16), cfg, 128, "v8")
+    assert torch.equal(fast.clamp_counts, ref.clamp_counts)
+    assert int(fast.clamp_counts.sum()) > 0
+    for u in range(U):
+        fa, fr = fast.code_arrays(u)
+        ra, rr = ref.code_arrays(u)
+        assert torch.equal(fa, ra), np.argwhere((fa != ra).cpu().numpy())[:5]
+        assert torch.equal(fr, rr)
+        ea, er, clamps = exact.encode(keys_f[u], s16[u], m, n, layout)
+        assert np.array_equal(fa.cpu().numpy(), ea) and np.array_equal(fr.cpu().numpy(), er)
+        assert int(fast.clamp_counts[u]) == clamps
+
+
+def test_fast_encoder_offset_fallback():
+    """A start token that is not a multiple of 16 (the fast kernel's stage
+    alignment) routes to encode_v8; the codes land at the offset unchanged."""
+    from paper_2502_00527_b200.codec import encode_device
+
+    keys = torch.from_numpy(_hard_keys(2, 700, seed=5)).to(torch.bfloat16).cuda()
+    cfg = pq.QuantConfig(4, 4)
+    kf = keys.float().cpu().numpy()
+    s16 = np.stack([exact.scales(kf[u], 4, 1) for u in range(2)])
+    a = _encode_raw(keys, s16, cfg, 64, "fast")
+    b = pq.PolarKVCache(cfg, 2, 128, 0, capacity=800, page_tokens=64, shuffle_pages=True)
+    b.scales16.copy_(a.scales16)
+    encode_device(keys, b.scales16, cfg, b.store_ref(), tok_offset_const=8)
+    torch.cuda.synchronize()
+    b.host_quant[:] = 708
+    for u in range(2):
+        for x, y in zip(a.code_arrays(u), b.code_arrays(u)):
+            assert torch.equal(x, y[8:])
