@@ -71,45 +71,111 @@ PQB_DEV uint32_t ef_m2_diag(float x, float y) {
 // Fast codes of one pair.  Returns the angle code (before the canonical
 // origin rule) and the rounded radius ratio rq; `worst` collects the
 // ambiguity metric (>= 0: inside a band), `rok` the magnitude-range check.
+// Octant-table index of a pair (m >= 3): the sign bits of x, y, |x| - |y| and
+// of the NB edge tests e_i, appended with funnel shifts (one SHF each).  The
+// table (ef_build_octant_table) maps it to the angle code.
 template <int M>
-PQB_DEV uint32_t ef_angle(float x, float y, float& worst) {
+__host__ __device__ constexpr int ef_index_bits() { return M == 2 ? 4 : 3 + (1 << (M - 3)); }
+
+template <int M>
+PQB_DEV uint32_t ef_angle(float x, float y, float& worst, const uint8_t* tab) {
   const float ax = fabsf(x), ay = fabsf(y);
   const float s = ax + ay, dif = ax - ay, a = fabsf(dif);
-  const uint32_t sx = __float_as_uint(x) >> 31, sy = __float_as_uint(y) >> 31;
-  constexpr int Q = 1 << (M - 2), H = 2 * Q;
-  int k0;
   if constexpr (M == 2) {
-    // the only edge is the diagonal: k0 = 1 iff |y| > |x|.  An exact tie
-    // |x| == |y| (frequent with bf16 keys) is decided by ef_m2_diag, not banded.
-    if (a == 0.0f) return ef_m2_diag(x, y);
-    worst = fmaxf(worst, fmaf(kQuadEdgeThr * 1.01f, s, -a));
-    k0 = dif < 0.0f ? 1 : 0;
+    // the only edge is the diagonal (swap bit).  An exact tie |x| == |y|
+    // (frequent with bf16 keys) is a fourth index bit: t = a - 2^-100 < 0 iff
+    // a == 0 (nonzero a >= 2^-75 in the safe magnitude range); ties are exact,
+    // so they are excluded from the band.
+    const float t = a - 0x1p-100f;
+    uint32_t idx = __funnelshift_l(__float_as_uint(x), 0u, 1);
+    idx = __funnelshift_l(__float_as_uint(y), idx, 1);
+    idx = __funnelshift_l(__float_as_uint(dif), idx, 1);
+    idx = __funnelshift_l(__float_as_uint(t), idx, 1);
+    worst = fmaxf(worst, fminf(fmaf(kQuadEdgeThr * 1.01f, s, -a), t));
+    return tab[idx];
   } else {
     constexpr int NB = 1 << (M - 3);
-    int kk = 0;
+    uint32_t idx = __funnelshift_l(__float_as_uint(x), 0u, 1);
+    idx = __funnelshift_l(__float_as_uint(y), idx, 1);
+    idx = __funnelshift_l(__float_as_uint(dif), idx, 1);
     float mn_e = INFINITY;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       const float e = fmaf(-a, ef_k(M, i), s);
-      kk += e > 0.0f ? 1 : 0;
+      idx = __funnelshift_l(__float_as_uint(e), idx, 1);
       mn_e = fminf(mn_e, fabsf(e));
     }
     worst = fmaxf(worst, fmaf(ef_band_max<M>(), s, -mn_e));
-    k0 = dif < 0.0f ? Q - kk : kk;
+    return tab[idx];
   }
-  const int base = sx ? (sy ? 0 : 2 * H) : H;
-  const int c = (sx ^ sy) ? base - k0 : base + k0;
-  return static_cast<uint32_t>(c) & (2u * H - 1u);
 }
 
-PQB_DEV float ef_radius(float x, float y, float inv, float& worst, bool& rok) {
-  const float r2 = fmaf(x, x, y * y);
-  rok &= in_safe_range_nonneg(r2);
-  const float q = r2 * rsqrt_approx(r2) * inv;
-  const float rq = rintf(q);
-  // |q - rq| >= 0.5 - 2^-18 q  <=>  band
-  worst = fmaxf(worst, fmaf(q, 0x1p-18f, fabsf(q - rq)) - 0.5f);
-  return rq;
+// Table of ef_angle (m >= 3): index = sx sy swap sign(e_0) .. sign(e_NB-1).
+// kk = edges the folded point lies above = NB - #(negative e_i); unfold as in
+// polar_math.cuh angle_code_fast.  (Non-monotone sign patterns cannot occur
+// outside the ambiguity band, which takes the exact path.)
+template <int M>
+PQB_DEV void ef_build_octant_table(uint8_t* tab, int tid, int nthreads) {
+  if constexpr (M == 2) {  // index = sx sy swap tie
+    for (int i = tid; i < 16; i += nthreads) {
+      const int sx = (i >> 3) & 1, sy = (i >> 2) & 1, swap = (i >> 1) & 1, tie = i & 1;
+      uint32_t c;
+      if (tie) {
+        c = ef_m2_diag(sx ? -1.0f : 1.0f, sy ? -1.0f : 1.0f);
+      } else {
+        const int base = sx ? (sy ? 0 : 4) : 2;
+        c = static_cast<uint32_t>((sx ^ sy) ? base - swap : base + swap) & 3u;
+      }
+      tab[i] = static_cast<uint8_t>(c);
+    }
+  } else {
+    constexpr int NB = 1 << (M - 3), Q = 1 << (M - 2), H = 2 * Q;
+    for (int i = tid; i < (1 << ef_index_bits<M>()); i += nthreads) {
+      const int sx = (i >> (NB + 2)) & 1, sy = (i >> (NB + 1)) & 1, swap = (i >> NB) & 1;
+      const int kk = NB - __popc(i & ((1 << NB) - 1));
+      const int k0 = swap ? Q - kk : kk;
+      const int base = sx ? (sy ? 0 : 2 * H) : H;
+      const int c = (sx ^ sy) ? base - k0 : base + k0;
+      tab[i] = static_cast<uint8_t>(c & (2 * H - 1));
+    }
+  }
+}
+
+// Packed fp32x2 arithmetic (FFMA2 / FMUL2 on sm_100a): two sub-vector pairs per
+// instruction, IEEE round-to-nearest per lane.
+struct F2 {
+  float x, y;
+};
+PQB_DEV F2 ffma2(F2 a, F2 b, F2 c) {
+  F2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+PQB_DEV F2 fmul2(F2 a, F2 b) {
+  F2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
+// rint(r / s) of two pairs (fast estimate, polar_math.cuh radius_raw_fast).
+// Band: |q - rq| >= 0.5 - 2^-18 q, tested as dq^2 >= 0.25 - 2^-18 q (a
+// superset: (0.5 - e)^2 >= 0.25 - e), so worst_r collects dq^2 + 2^-18 q - 0.25.
+PQB_DEV void ef_radius2(F2 x, F2 y, F2 inv, float& rq0, float& rq1, float& worst_r, bool& rok) {
+  const F2 r2 = ffma2(x, x, fmul2(y, y));
+  rok &= in_safe_range_nonneg(r2.x) & in_safe_range_nonneg(r2.y);
+  const F2 q = fmul2(fmul2(r2, F2{rsqrt_approx(r2.x), rsqrt_approx(r2.y)}), inv);
+  const F2 rq{rintf(q.x), rintf(q.y)};
+  const F2 dq = ffma2(rq, F2{-1.0f, -1.0f}, q);  // exact
+  const F2 m = ffma2(dq, dq, ffma2(q, F2{0x1p-18f, 0x1p-18f}, F2{-0.25f, -0.25f}));
+  worst_r = fmaxf(worst_r, fmaxf(m.x, m.y));
+  rq0 = rq.x;
+  rq1 = rq.y;
 }
 
 // Word w (0 <= w < 2B) of a token row of B-bit codes when lane-in-row j holds
@@ -163,10 +229,24 @@ PQB_DEV void ef_pack(const uint32_t (&ac)[8], const float (&rq)[8], uint32_t kee
     clamps += __saturatef(rq[i] - kTop);  // 1 iff rq >= top + 1 (integers)
     const float rc = fminf(rq[i], kTop);
     cr += __float_as_uint(rc + 12582912.0f) << (N * i);
-    const uint32_t a = rc == 0.0f ? (1u << (M - 1)) : ac[i];  // polar_codec.py:297
-    ca += a << (M * i);
+    if constexpr (M == N) {
+      ca += ac[i] << (M * i);
+    } else {
+      const uint32_t a = rc == 0.0f ? (1u << (M - 1)) : ac[i];  // polar_codec.py:297
+      ca += a << (M * i);
+    }
   }
   cr -= kMagicSum;
+  if constexpr (M == N) {
+    // canonical origin angle (polar_codec.py:297) on whole words: fields whose
+    // radius code is 0 get angle 2^(M-1)
+    constexpr uint32_t kLow = M == 4 ? 0x11111111u : (M == 3 ? 0x00249249u : 0x00005555u);
+    uint32_t t = cr | (cr >> 1);
+    if constexpr (M >= 3) t |= cr >> 2;
+    if constexpr (M == 4) t |= cr >> 3;
+    const uint32_t z = (t & kLow) ^ kLow;  // bit 0 of each zero field
+    ca = (ca & ~(z * ((1u << M) - 1u))) | (z << (M - 1));
+  }
   ca &= keep_a;  // zero-scale channels: both codes 0 (polar_codec.py:298-301)
   cr &= keep_r;
 }
@@ -184,6 +264,9 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
   constexpr int kStagesPerItem = kEfItemTok / kStageTok;
   extern __shared__ __align__(128) uint8_t esm[];
   __shared__ uint64_t bars_all[kEfWarps][kEfStages];
+  __shared__ uint8_t octant_tab[64];
+  ef_build_octant_table<M>(octant_tab, threadIdx.x, blockDim.x);
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = lane >> 3, cg = lane & 7;
   uint64_t* bars = bars_all[warp];
@@ -322,14 +405,15 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
         }
         uint32_t ac[8];
         float rq[8];
-        float worst = -1.0f;
+        float worst = -1.0f, worst_r = -1.0f;
         bool rok = true;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          rq[i] = ef_radius(x[i], y[i], inv[i], worst, rok);
-          ac[i] = ef_angle<M>(x[i], y[i], worst);
+        for (int i = 0; i < 8; i += 2) {
+          ef_radius2(F2{x[i], x[i + 1]}, F2{y[i], y[i + 1]}, F2{inv[i], inv[i + 1]}, rq[i], rq[i + 1], worst_r, rok);
+          ac[i] = ef_angle<M>(x[i], y[i], worst, octant_tab);
+          ac[i + 1] = ef_angle<M>(x[i + 1], y[i + 1], worst, octant_tab);
         }
-        if (!(worst < 0.0f) || !rok) {
+        if (!(fmaxf(worst, worst_r) < 0.0f) || !rok) {
           // rare: the exact pipeline for this lane's eight pairs (zero-scale
           // channels are masked in ef_pack and need no exact work)
 #pragma unroll
