@@ -139,11 +139,13 @@ class ClockSampler:
                 "reasons": sorted(n for b, n in self.REASONS.items() if bits & b), "samples": len(self.samples)}
 
 
-def unit_bytes(T: int, G: int, d: int, m: int, n: int) -> int:
+def unit_bytes(T: int, G: int, d: int, m: int, n: int, value_bits: int | None = None) -> int:
     """Algorithmic HBM bytes of one (sequence, layer, kv-head) unit per decode
-    step: codes once per KV head, V once (bf16), fp16 scales,
-    bf16 q in / bf16 out for the G query heads."""
-    return T * (d // 2) * (m + n) // 8 + T * d * 2 + (d // 2) * 2 + 2 * G * d * 2
+    step: codes once per KV head, V once (bf16, or 4-bit codes +
+    fp32 (zp, scale) per token in the value-quantized mode), fp16 scales, bf16
+    q in / bf16 out for the G query heads."""
+    v = T * d * 2 if value_bits is None else T * (d * value_bits // 8 + 8)
+    return T * (d // 2) * (m + n) // 8 + v + (d // 2) * 2 + 2 * G * d * 2
 
 
 # ------------------------------------------------------------- CPU baseline
@@ -208,7 +210,8 @@ class DecodeWorkload:
     layers x (batch x kv_heads) units, each with T tokens; one step runs every
     layer's fused decode (optionally followed by the head-output gather)."""
 
-    def __init__(self, dev, *, layers, batch, hq, hkv, T, m, n, page_tokens, seed, plan=None, group=None):
+    def __init__(self, dev, *, layers, batch, hq, hkv, T, m, n, page_tokens, seed, plan=None, group=None,
+                 value_bits=None):
         import torch
 
         import paper_2502_00527_b200 as pq
@@ -220,8 +223,9 @@ class DecodeWorkload:
         self.upl = plan.units_per_layer if plan is not None else batch * hkv
         self.batch, self.hq = batch, hq
         cfg = pq.QuantConfig(m, n)
+        self.value_bits = value_bits
         self.cache = pq.PolarKVCache(cfg, layers * self.upl, 128, 0, capacity=T, page_tokens=page_tokens,
-                                     value_dtype=torch.bfloat16, device=dev)
+                                     value_dtype=torch.bfloat16, device=dev, value_bits=value_bits)
         syn = pq.SyntheticConfig(T, 128, outlier_channels=frozenset({0, 1}))
         chunk = max(1, min(self.upl, (1 << 31) // (T * 128 * 2)))  # <= 2 GB bf16 staging per tensor
         for layer in range(layers):
@@ -253,7 +257,7 @@ class DecodeWorkload:
         return self.L  # one fused decode launch per layer (split merge inside)
 
     def bytes_per_launch(self) -> int:
-        return self.upl * unit_bytes(self.T, self.G, 128, self.m, self.n)
+        return self.upl * unit_bytes(self.T, self.G, 128, self.m, self.n, self.value_bits)
 
     def capture(self, fn):
         torch = self.torch
@@ -402,6 +406,9 @@ def run_extras(dev, a) -> dict:
         "configs[0]_L1_B1_4K_m4n4": dict(layers=1, batch=1, hq=32, hkv=8, T=4096, m=4, n=4),
         "configs[2]_P1_L32_B8_128K_m3n2": dict(layers=32, batch=8, hq=32, hkv=8, T=131072, m=3, n=2),
         "configs[3]_per_gpu_L80_B32_32K_G8_1kvhead": dict(layers=80, batch=32, hq=8, hkv=1, T=32768, m=4, n=4),
+        # configs[1] with the reference's value-quantization mode
+        # (PackedKVCache(quantize_values=True, value_bits=4)) read inside the kernel
+        "configs[1]_vq4_values": dict(layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, value_bits=4),
     }
     for name, s in specs.items():
         try:

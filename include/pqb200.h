@@ -60,6 +60,13 @@ extern "C" {
 #define PQB_F32 0
 #define PQB_BF16 1
 #define PQB_F16 2
+/* pqb_store.value_dtype only: 4-bit per-token uniform value codes
+ * (quantize_uniform PER_TOKEN, baseline_quant.py:58-110; the reference's
+ * PackedKVCache(quantize_values=True, value_bits=4), kv_cache.py:199-209).
+ * Value region of a page (d = 128): [page_tokens/32 tiles][2048 B codes in
+ * MMA-fragment order, see INTEGRATION.md] then [page_tokens][zp, scale] fp32.
+ * Read back: fl(fl(code * scale) + zp) (dequantize_uniform, :143-167). */
+#define PQB_VQ4 16
 
 /* pairing layouts: same numeric values as PairingLayout (tensor_core.py:41-50) */
 #define PQB_ADJACENT 0
@@ -83,7 +90,7 @@ typedef struct pqb_store {
   const int32_t* page_table;
   int32_t max_pages;
   int32_t page_tokens;
-  int32_t value_dtype; /* PQB_F32 or PQB_BF16 */
+  int32_t value_dtype; /* PQB_F32, PQB_BF16 or PQB_VQ4 */
   int32_t reserved;
 } pqb_store;
 
@@ -144,6 +151,12 @@ int pqb_encode(const void* keys, int key_dtype, int64_t n_units, int64_t tokens,
 int pqb_store_values(const void* values, int value_dtype, int64_t n_units, int64_t tokens, int d,
                      int64_t unit_stride, int64_t tok_stride, const pqb_store* store,
                      const int32_t* tok_offset, int64_t tok_offset_const, pqb_stream_t stream);
+/* Same, with a device flag word: non-finite values are OR-ed in as
+ * PQB_FLAG_NONFINITE (quantize_uniform raises on them, baseline_quant.py:88-89;
+ * checked for PQB_VQ4 stores). */
+int pqb_store_values_ex(const void* values, int value_dtype, int64_t n_units, int64_t tokens, int d,
+                        int64_t unit_stride, int64_t tok_stride, const pqb_store* store, const int32_t* tok_offset,
+                        int64_t tok_offset_const, int32_t* flags, pqb_stream_t stream);
 
 /* Write full-precision keys [n_units][tokens][d] into the residual ring at
  * token indices tok_offset_const + t (prefill's residual tail, kv_cache.py:175-176). */

@@ -195,6 +195,29 @@ def attend(weights: np.ndarray, values: np.ndarray) -> np.ndarray:
     return weights @ np.asarray(values, dtype=np.float64)
 
 
+def quantize_values(values: np.ndarray, bits: int):
+    """quantize_uniform(values, bits, PER_TOKEN), baseline_quant.py:58-66, 69-110:
+    per row zp = min, scale = fl32(fl32(max - zp) / (2^b - 1)),
+    code = clip(rint(fl32(fl32(v - zp) / scale)), 0, 2^b - 1) (scale 0 -> 0).
+    Returns (codes uint8 [T, d], zero_point [T], scale [T]) in float32."""
+    v = np.asarray(values, dtype=np.float32)
+    top = (1 << bits) - 1
+    zp = v.min(axis=1, keepdims=True)
+    scale = (v.max(axis=1, keepdims=True) - zp) / np.float32(top)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        raw = np.rint((v - zp) / scale)
+    raw = np.where(scale == 0.0, np.float32(0.0), raw)
+    codes = np.clip(raw, 0, top).astype(np.uint8)
+    return codes, zp[:, 0].astype(np.float32), scale[:, 0].astype(np.float32)
+
+
+def dequantize_values(codes: np.ndarray, zero_point: np.ndarray, scale: np.ndarray) -> np.ndarray:
+    """dequantize_uniform PER_TOKEN, baseline_quant.py:143-167: fl32(fl32(code * scale) + zp)."""
+    c = np.asarray(codes).astype(np.float32)
+    return (c * np.asarray(scale, np.float32)[:, None] + np.asarray(zero_point, np.float32)[:, None]).astype(
+        np.float32)
+
+
 # ------------------------------------------------------------ the cache
 
 

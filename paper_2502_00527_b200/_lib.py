@@ -17,6 +17,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libpqb200.so"
 PQB_OK, PQB_EINVAL, PQB_ESTATE, PQB_ECUDA, PQB_EUNSUPPORTED = 0, 1, 2, 3, 4
 PQB_FLAG_NONFINITE, PQB_FLAG_SCALE_OVERFLOW = 1, 2
 PQB_F32, PQB_BF16, PQB_F16 = 0, 1, 2
+PQB_VQ4 = 16  # pqb_store.value_dtype: 4-bit per-token value codes
 PQB_DECODE_FORCE_GENERIC, PQB_DECODE_NO_COMBINE, PQB_DECODE_DQ, PQB_DECODE_LUT = 1, 2, 4, 8
 PQB_DECODE_PROBE_MEM, PQB_DECODE_PROBE_COMPUTE = 64, 128
 
@@ -79,6 +80,10 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "pqb_store_values": (
         c_i32,
         [c_vp, c_i32, c_i64, c_i64, c_i32, c_i64, c_i64, ctypes.POINTER(PqbStore), c_vp, c_i64, c_vp],
+    ),
+    "pqb_store_values_ex": (
+        c_i32,
+        [c_vp, c_i32, c_i64, c_i64, c_i32, c_i64, c_i64, ctypes.POINTER(PqbStore), c_vp, c_i64, c_vp, c_vp],
     ),
     "pqb_store_residual": (
         c_i32,

@@ -68,6 +68,7 @@ class PolarKVCache:
         device=None,
         shuffle_pages: bool = False,
         seed: int = 0,
+        value_bits: int | None = None,
     ) -> None:
         if residual_len < 0:
             raise ValueError(f"residual_len must be >= 0, got {residual_len}")
@@ -77,6 +78,13 @@ class PolarKVCache:
             raise ValueError(f"page_tokens must be a positive multiple of 32, got {page_tokens}")
         if value_dtype not in (torch.float32, torch.bfloat16):
             raise ValueError("value_dtype must be torch.float32 or torch.bfloat16")
+        if value_bits is not None:
+            # per-token uniform value codes (PackedKVCache(quantize_values=True), kv_cache.py:199-209)
+            if not 1 <= int(value_bits) <= 8:
+                raise ValueError(f"bits must be in [1, 8], got {value_bits}")
+            if int(value_bits) != 4 or dim != 128:
+                raise ValueError("the batched cache stores quantized values as 4-bit codes with dim = 128 "
+                                 f"(got value_bits={value_bits}, dim={dim})")
         self.device = require_cuda(device)
         self.cfg = cfg
         self.n_units = int(n_units)
@@ -84,13 +92,17 @@ class PolarKVCache:
         self.residual_len = int(residual_len)
         self.page_tokens = int(page_tokens)
         self.value_dtype = value_dtype
+        self.value_bits = None if value_bits is None else int(value_bits)
         self.shuffle_pages = shuffle_pages
         self._seed = seed
         half = dim // 2
         P = self.page_tokens
         a_bytes = P * half * cfg.angle_bits // 8
         r_bytes = P * half * cfg.radius_bits // 8
-        v_bytes = P * dim * (4 if value_dtype == torch.float32 else 2)
+        if self.value_bits is not None:
+            v_bytes = P * 64 + P * 8  # 4-bit codes (MMA-fragment order) + (zp, scale) fp32 per token
+        else:
+            v_bytes = P * dim * (4 if value_dtype == torch.float32 else 2)
         self.angle_off = 0
         self.radius_off = round_up(a_bytes, 128)
         self.value_off = round_up(self.radius_off + r_bytes, 128)
@@ -142,7 +154,8 @@ class PolarKVCache:
             page_table=ptr(self.page_table),
             max_pages=self.max_pages,
             page_tokens=self.page_tokens,
-            value_dtype=_lib.PQB_F32 if self.value_dtype == torch.float32 else _lib.PQB_BF16,
+            value_dtype=(_lib.PQB_VQ4 if self.value_bits is not None
+                         else _lib.PQB_F32 if self.value_dtype == torch.float32 else _lib.PQB_BF16),
             reserved=0,
         )
         self._struct = _lib.PqbCache(
@@ -195,6 +208,8 @@ class PolarKVCache:
     @property
     def bytes_per_token(self) -> int:
         half = self.dim // 2
+        if self.value_bits is not None:
+            return half * (self.cfg.angle_bits + self.cfg.radius_bits) // 8 + self.dim // 2 + 8
         vb = 4 if self.value_dtype == torch.float32 else 2
         return half * (self.cfg.angle_bits + self.cfg.radius_bits) // 8 + self.dim * vb
 
@@ -251,9 +266,9 @@ class PolarKVCache:
         if v is not None and v.stride(-1) != 1:
             v = v.contiguous()
         _lib.call(
-            "pqb_store_values", ptr(v), dtype_code(v) if v is not None else 0, n, T, self.dim,
+            "pqb_store_values_ex", ptr(v), dtype_code(v) if v is not None else 0, n, T, self.dim,
             v.stride(0) if v is not None else 0, v.stride(1) if v is not None else 0, ctypes.byref(sub.store),
-            None, 0, stream_ptr(self.device),
+            None, 0, ptr(self.flags), stream_ptr(self.device),
         )
         self.seq_lens[u0:u1].fill_(T)
         self.quant_lens[u0:u1].fill_(boundary)

@@ -63,8 +63,12 @@ static int check_store(const pqb_store* st, int d, int m, int n, bool need_value
             "store: radius region exceeds page");
   if (need_values) {
     PQB_CHECK(st->value_off >= 0, PQB_EINVAL, "store: no value region");
-    PQB_CHECK(st->value_dtype == PQB_F32 || st->value_dtype == PQB_BF16, PQB_EINVAL, "store: bad value dtype");
-    const int64_t vb = static_cast<int64_t>(st->page_tokens) * d * (st->value_dtype == PQB_F32 ? 4 : 2);
+    PQB_CHECK(st->value_dtype == PQB_F32 || st->value_dtype == PQB_BF16 || st->value_dtype == PQB_VQ4, PQB_EINVAL,
+              "store: bad value dtype");
+    PQB_CHECK(st->value_dtype != PQB_VQ4 || (d == 128 && st->value_off % 16 == 0), PQB_EUNSUPPORTED,
+              "store: 4-bit values need d = 128 and a 16-byte aligned value region");
+    const int64_t vb = static_cast<int64_t>(st->page_tokens) *
+                       (st->value_dtype == PQB_VQ4 ? 72 : d * (st->value_dtype == PQB_F32 ? 4 : 2));
     PQB_CHECK(st->value_off + vb <= st->page_bytes, PQB_EINVAL, "store: value region exceeds page");
   }
   return PQB_OK;
@@ -132,14 +136,24 @@ int pqb_encode(const void* keys, int key_dtype, int64_t n_units, int64_t tokens,
 int pqb_store_values(const void* values, int value_dtype, int64_t n_units, int64_t tokens, int d,
                      int64_t unit_stride, int64_t tok_stride, const pqb_store* store, const int32_t* tok_offset,
                      int64_t tok_offset_const, pqb_stream_t stream) {
+  return pqb_store_values_ex(values, value_dtype, n_units, tokens, d, unit_stride, tok_stride, store, tok_offset,
+                             tok_offset_const, nullptr, stream);
+}
+
+int pqb_store_values_ex(const void* values, int value_dtype, int64_t n_units, int64_t tokens, int d,
+                        int64_t unit_stride, int64_t tok_stride, const pqb_store* store, const int32_t* tok_offset,
+                        int64_t tok_offset_const, int32_t* flags, pqb_stream_t stream) {
   PQB_CHECK(d >= 2 && d % 2 == 0, PQB_EINVAL, "vector dimension must be even and >= 2, got %d", d);
   PQB_CHECK(values == nullptr || dtype_ok(value_dtype), PQB_EINVAL, "bad value dtype");
   PQB_CHECK(store && store->pool && store->value_off >= 0, PQB_EINVAL, "store has no value region");
-  PQB_CHECK(store->value_dtype == PQB_F32 || store->value_dtype == PQB_BF16, PQB_EINVAL, "bad store value dtype");
+  PQB_CHECK(store->value_dtype == PQB_F32 || store->value_dtype == PQB_BF16 || store->value_dtype == PQB_VQ4,
+            PQB_EINVAL, "bad store value dtype");
+  PQB_CHECK(store->value_dtype != PQB_VQ4 || (d == 128 && tok_offset == nullptr && tok_offset_const % 32 == 0),
+            PQB_EUNSUPPORTED, "4-bit value stores take d = 128 and whole 32-token tiles");
   PQB_CHECK(n_units >= 0 && n_units <= 65535 && tokens >= 0, PQB_EINVAL, "bad token / unit count");
   if (n_units == 0 || tokens == 0) return PQB_OK;
   launch_store_values(values, value_dtype, n_units, tokens, d, unit_stride, tok_stride, *store, tok_offset,
-                      tok_offset_const, reinterpret_cast<cudaStream_t>(stream));
+                      tok_offset_const, reinterpret_cast<cudaStream_t>(stream), flags);
   return cuda_status("pqb_store_values");
 }
 

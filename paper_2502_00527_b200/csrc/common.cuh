@@ -100,6 +100,34 @@ PQB_DEV int64_t value_offset(int64_t t, int e, int d, int value_dtype) {
   return (t * d + e) * 2;
 }
 
+// PQB_VQ4 value pages (d = 128).  Tile = 32 tokens; its 4096 codes are 512
+// words in m16n8k16 A-fragment order of V^T (rows = dims, cols = tokens):
+// word (mt * 2 + ks) * 32 + lane holds, for lane = 4 g + t, the fragment
+// registers a0..a3 of dim block mt and token block ks as nibbles
+//   a_k low half  (token 2t + 8 (k >> 1), dim g + 8 (k & 1)) at bits 4k
+//   a_k high half (token 2t + 1 + 8 (k >> 1), same dim)      at bits 16 + 4k.
+PQB_DEV void vq4_pos(int t_in_tile, int e, int& word, int& shift) {
+  const int ks = t_in_tile >> 4, tt = t_in_tile & 15, mt = e >> 4, ee = e & 15;
+  const int k = (ee >> 3) + 2 * (tt >> 3);
+  word = (mt * 2 + ks) * 32 + (ee & 7) * 4 + ((tt & 7) >> 1);
+  shift = 4 * k + 16 * (tt & 1);
+}
+PQB_DEV int64_t vq4_params_off(const pqb_store& st) { return st.value_off + static_cast<int64_t>(st.page_tokens) * 64; }
+
+// Value (token t of the page, element e) of any value store, as fp32.
+PQB_DEV float load_value(const pqb_store& st, const uint8_t* page, int64_t t, int e, int d) {
+  if (st.value_dtype == PQB_VQ4) {
+    int w, sh;
+    vq4_pos(static_cast<int>(t & 31), e, w, sh);
+    const uint32_t word = reinterpret_cast<const uint32_t*>(page + st.value_off + (t >> 5) * 2048)[w];
+    const float2 zs = reinterpret_cast<const float2*>(page + vq4_params_off(st))[t];
+    return __fadd_rn(__fmul_rn(static_cast<float>((word >> sh) & 15u), zs.y), zs.x);
+  }
+  const uint8_t* vp = page + st.value_off + value_offset(t, e, d, st.value_dtype);
+  return st.value_dtype == PQB_F32 ? *reinterpret_cast<const float*>(vp)
+                                   : __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(vp));
+}
+
 // ---------------------------------------------------------------- warp ops
 
 PQB_DEV float warp_max(float v) {

@@ -432,13 +432,11 @@ __global__ void __launch_bounds__(256)
     for (int t = 0; t < nvalid; ++t) {
       const int64_t ta = static_cast<int64_t>(tile) * kTile + t;
       const int64_t page = ta / P, in_page = ta - page * P;
-      const uint8_t* vreg = page_base_c(c.store, unit, page) + c.store.value_off;
+      const uint8_t* pg = page_base_c(c.store, unit, page);
       for (int k = 0; k < dpl; ++k) {
         const int e = lane + 32 * k;
         if (e < d) {
-          const uint8_t* vp = vreg + value_offset(in_page, e, d, c.store.value_dtype);
-          const float v = c.store.value_dtype == PQB_F32 ? *reinterpret_cast<const float*>(vp)
-                                                         : __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(vp));
+          const float v = load_value(c.store, pg, in_page, e, d);
           for (int g = 0; g < G; ++g) o[g][k] = fmaf(pbuf[t * G + g], v, o[g][k]);
         }
       }
@@ -647,7 +645,8 @@ static int dispatch_fast(const DecodeArgs& a, cudaStream_t s, bool& handled) {
 
 int launch_decode(const DecodeArgs& a, cudaStream_t s) {
   const pqb_cache& c = *a.cache;
-  const bool fast_ok = c.d == 128 && (a.out == nullptr || c.store.value_dtype == PQB_BF16) &&
+  const bool vq = c.store.value_dtype == PQB_VQ4 && a.out != nullptr;  // 4-bit values: DQ kernel or generic
+  const bool fast_ok = c.d == 128 && (a.out == nullptr || c.store.value_dtype == PQB_BF16 || vq) &&
                        (a.group == 1 || a.group == 4 || a.group == 8) && c.store.page_tokens % kTile == 0 &&
                        (c.store.angle_off % 16 == 0) && (c.store.radius_off % 16 == 0) &&
                        (c.store.value_off % 16 == 0 || a.out == nullptr) && (c.store.page_bytes % 16 == 0) &&
@@ -657,7 +656,7 @@ int launch_decode(const DecodeArgs& a, cudaStream_t s) {
     const int rc = launch_dq_path(a, s, handled);
     if (rc != PQB_OK) return rc;
   }
-  if (fast_ok && !handled && !(a.flags & PQB_DECODE_FORCE_GENERIC)) {
+  if (fast_ok && !handled && !vq && !(a.flags & PQB_DECODE_FORCE_GENERIC)) {
     // scores requested -> the bit-exact scoring sequence; fused-only -> FMA form
     const int rc = a.scores != nullptr ? dispatch_fast<true>(a, s, handled) : dispatch_fast<false>(a, s, handled);
     if (rc != PQB_OK) return rc;

@@ -49,11 +49,12 @@
 
 namespace pqb {
 
-template <int G, int M, int N>
+template <int G, int M, int N, int VQ = 0>
 struct DqCfg {
   static constexpr int kABytes = kTile * 8 * M;
   static constexpr int kRBytes = kTile * 8 * N;
-  static constexpr int kVBytes = kTile * 256;
+  // bf16 value rows, or (VQ) 2 KB of fragment-order 4-bit codes + 32 (zp, scale)
+  static constexpr int kVBytes = VQ ? 2048 + kTile * 8 : kTile * 256;
   static constexpr int kStageBytes = kABytes + kRBytes + kVBytes;
   static constexpr int kPBytes = kTile * 8 * 4;              // fp32 [32 tokens][8 queries] residual-dot scratch
   static constexpr int kTabBytes = 128 << (M + N);          // product table, 16 bank-slot copies
@@ -169,11 +170,30 @@ PQB_DEV uint2 lds_u2(uint32_t addr) {
 // PROBE (diagnostics only, flags PQB_DECODE_PROBE_*): 0 = the kernel; 1 = memory
 // only (tiles stream through the ring, no compute); 2 = compute only (every tile
 // is re-read from the unit's first page, i.e. from L2).
-template <int G, int M, int N, int PROBE = 0>
+// VQ: PQB_VQ4 value pages (kv_cache.py:199-209 quantize_values): the P.V MMA
+// takes the 4-bit codes as exact bf16 integers (A) against P * scale (B, hi/lo),
+// and the zero points join as sum_t p_t zp_t per query:
+//   o = sum_t p_t (c_t s_t + z_t) = [codes] . (p s) + sum_t p_t z_t.
+template <int M, int N, int VQ>
+PQB_DEV void issue_tile_dq(uint8_t* st, const pqb_store& s, const uint8_t* pb, int tile, int tpp, uint64_t* bar) {
+  if constexpr (!VQ) {
+    issue_tile<M, N>(st, s, pb, tile, tpp, true, bar);
+  } else {
+    constexpr uint32_t kA = kTile * 8 * M, kR = kTile * 8 * N;
+    const int tin = tile % tpp, in_page = tin * kTile;
+    mbar_arrive_expect_tx(bar, kA + kR + 2048 + kTile * 8);
+    bulk_g2s(st, pb + s.angle_off + in_page * 8 * M, kA, bar);
+    bulk_g2s(st + kA, pb + s.radius_off + in_page * 8 * N, kR, bar);
+    bulk_g2s(st + kA + kR, pb + s.value_off + static_cast<int64_t>(tin) * 2048, 2048, bar);
+    bulk_g2s(st + kA + kR + 2048, pb + vq4_params_off(s) + static_cast<int64_t>(in_page) * 8, kTile * 8, bar);
+  }
+}
+
+template <int G, int M, int N, int PROBE = 0, int VQ = 0>
 __global__ void __launch_bounds__(kNW * 32, 1)
     decode_dq_kernel(const pqb_cache c, const void* __restrict__ q, int q_dtype, float sm_scale_log2, EpiArgs ep,
                      WorkSplit ws) {
-  using Cfg = DqCfg<G, M, N>;
+  using Cfg = DqCfg<G, M, N, VQ>;
   constexpr bool kFused = M == 4 && N == 4;
   constexpr bool kPacked = Cfg::kPacked;
   static_assert(G == 1 || G == 2 || G == 4 || G == 8, "G");
@@ -290,13 +310,14 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         if (tile < t_hi) {
           fence_proxy_async_smem();
           const uint32_t sl = (k_iter + s) % kStages;
-          issue_tile<M, N>(my_area + sl * Cfg::kStageBytes, c.store,
-                           page_base_c(c.store, unit, PROBE == 2 ? 0 : tile / tpp), PROBE == 2 ? 0 : tile, tpp, true,
-                           bar + sl);
+          issue_tile_dq<M, N, VQ>(my_area + sl * Cfg::kStageBytes, c.store,
+                                  page_base_c(c.store, unit, PROBE == 2 ? 0 : tile / tpp), PROBE == 2 ? 0 : tile, tpp,
+                                  bar + sl);
         }
       }
     }
     float m_run = -INFINITY, l_run = 0.0f;  // query g8 (lanes g8 < G)
+    float z_run = 0.0f;                     // VQ: sum_t p_t zp_t of query g8 (lane partial)
     float d[8][4];
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt)
@@ -313,8 +334,8 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         __syncwarp();
         if (lane == 0 && nt < t_hi) {
           fence_proxy_async_smem();
-          issue_tile<M, N>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, nt / tpp), nt, tpp,
-                           true, bar + s);
+          issue_tile_dq<M, N, VQ>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, nt / tpp), nt,
+                                  tpp, bar + s);
         }
         continue;
       }
@@ -388,12 +409,19 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       const float alpha = fast_exp2(m_run - mn);
       const bool rescale = mn != m_run;
       m_run = mn;
-      float ls = 0.0f;
+      float ls = 0.0f, zs = 0.0f;
       uint32_t phi[4], plo[4];  // bf16x2 (tokens 8 nb + 2 t4, +1)
 #pragma unroll
       for (int nb = 0; nb < 4; ++nb) {
-        const float p0 = fast_exp2(x[nb][0] - mn), p1 = fast_exp2(x[nb][1] - mn);
+        float p0 = fast_exp2(x[nb][0] - mn), p1 = fast_exp2(x[nb][1] - mn);
         ls += p0 + p1;
+        if constexpr (VQ) {  // (zp, scale) of tokens 8 nb + 2 t4, +1
+          const float4 zsv =
+              reinterpret_cast<const float4*>(st + Cfg::kABytes + Cfg::kRBytes + 2048)[4 * nb + t4];
+          zs = fmaf(p0, zsv.x, fmaf(p1, zsv.z, zs));
+          p0 *= zsv.y;
+          p1 *= zsv.w;
+        }
         const __nv_bfloat162 hi = __floats2bfloat162_rn(p0, p1);
         const float2 hf = __bfloat1622float2(hi);
         const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
@@ -401,6 +429,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         plo[nb] = *reinterpret_cast<const uint32_t*>(&lo);
       }
       l_run = fmaf(l_run, alpha, ls);
+      if constexpr (VQ) z_run = fmaf(z_run, alpha, zs);
       if (__any_sync(0xffffffffu, rescale && g8 < G)) {
         const float a0 = __shfl_sync(0xffffffffu, alpha, qc0 * 4), a1 = __shfl_sync(0xffffffffu, alpha, qc1 * 4);
 #pragma unroll
@@ -420,23 +449,46 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       }
       // ---- P.V on tensor cores: O^T[128 x 8] += V^T[128 x 32] . P^T[32 x 8];
       // the P^T B-fragments are the score registers (k-step ks = n-blocks 2ks, 2ks+1)
-      const uint32_t vbase = smem_u32(st + Cfg::kABytes + Cfg::kRBytes) + ld_row;
+      if constexpr (VQ) {
+        // A fragments straight from the code words: nibble -> bf16 (128 + c) by
+        // OR-ing into the exponent pattern of 128, then - 128 (exact)
+        const uint32_t* vw = reinterpret_cast<const uint32_t*>(st + Cfg::kABytes + Cfg::kRBytes);
+        const __nv_bfloat162 k128 = __floats2bfloat162_rn(128.0f, 128.0f);
 #pragma unroll
-      for (int mt = 0; mt < 8; ++mt) {
+        for (int mt = 0; mt < 8; ++mt) {
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks) {
-          uint32_t a0, a1, a2, a3;
-          ldsm_x4_trans(vbase + ks * 16 * 256 + (ld_chunk ^ (mt << 5)), a0, a1, a2, a3);
-          mma_bf16(d[mt], a0, a1, a2, a3, phi[2 * ks], phi[2 * ks + 1]);
-          if constexpr (!kPacked) mma_bf16(d[mt], a0, a1, a2, a3, plo[2 * ks], plo[2 * ks + 1]);
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint32_t w = vw[(mt * 2 + ks) * 32 + lane];
+            uint32_t a[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t b = ((w >> (4 * k)) & 0x000F000Fu) | 0x43004300u;
+              const __nv_bfloat162 v = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&b), k128);
+              a[k] = *reinterpret_cast<const uint32_t*>(&v);
+            }
+            mma_bf16(d[mt], a[0], a[1], a[2], a[3], phi[2 * ks], phi[2 * ks + 1]);
+            if constexpr (!kPacked) mma_bf16(d[mt], a[0], a[1], a[2], a[3], plo[2 * ks], plo[2 * ks + 1]);
+          }
+        }
+      } else {
+        const uint32_t vbase = smem_u32(st + Cfg::kABytes + Cfg::kRBytes) + ld_row;
+#pragma unroll
+        for (int mt = 0; mt < 8; ++mt) {
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4_trans(vbase + ks * 16 * 256 + (ld_chunk ^ (mt << 5)), a0, a1, a2, a3);
+            mma_bf16(d[mt], a0, a1, a2, a3, phi[2 * ks], phi[2 * ks + 1]);
+            if constexpr (!kPacked) mma_bf16(d[mt], a0, a1, a2, a3, plo[2 * ks], plo[2 * ks + 1]);
+          }
         }
       }
       __syncwarp();
       if (lane == 0 && nt < t_hi) {
         fence_proxy_async_smem();
-        issue_tile<M, N>(my_area + s * Cfg::kStageBytes, c.store,
-                         page_base_c(c.store, unit, PROBE == 2 ? 0 : nt / tpp), PROBE == 2 ? 0 : nt, tpp, true,
-                         bar + s);
+        issue_tile_dq<M, N, VQ>(my_area + s * Cfg::kStageBytes, c.store,
+                                page_base_c(c.store, unit, PROBE == 2 ? 0 : nt / tpp), PROBE == 2 ? 0 : nt, tpp,
+                                bar + s);
       }
     }
 
@@ -448,6 +500,18 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
         for (int k = 0; k < 4; ++k) d[mt][k] += __shfl_xor_sync(0xffffffffu, d[mt][k], 2);
+    }
+    if constexpr (VQ) {  // + sum_t p_t zp_t of the column's query
+      z_run += __shfl_xor_sync(0xffffffffu, z_run, 1);
+      z_run += __shfl_xor_sync(0xffffffffu, z_run, 2);
+      const float z0 = __shfl_sync(0xffffffffu, z_run, qc0 * 4), z1 = __shfl_sync(0xffffffffu, z_run, qc1 * 4);
+#pragma unroll
+      for (int mt = 0; mt < 8; ++mt) {
+        d[mt][0] += z0;
+        d[mt][1] += z1;
+        d[mt][2] += z0;
+        d[mt][3] += z1;
+      }
     }
     __syncthreads();
     float* red = reinterpret_cast<float*>(warp_area);
@@ -474,19 +538,19 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 
 // ------------------------------------------------------------------ host side
 
-template <int G, int M, int N, int PROBE = 0>
+template <int G, int M, int N, int PROBE = 0, int VQ = 0>
 static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s) {
-  using Cfg = DqCfg<G, M, N>;
+  using Cfg = DqCfg<G, M, N, VQ>;
   static bool attr_set = false;
   if (!attr_set) {
-    if (cudaFuncSetAttribute(decode_dq_kernel<G, M, N, PROBE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(decode_dq_kernel<G, M, N, PROBE, VQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg::kSmem) != cudaSuccess) {
       set_error("cudaFuncSetAttribute(smem=%d) failed", Cfg::kSmem);
       return PQB_ECUDA;
     }
     attr_set = true;
   }
-  decode_dq_kernel<G, M, N, PROBE>
+  decode_dq_kernel<G, M, N, PROBE, VQ>
       <<<grid, kNW * 32, Cfg::kSmem, s>>>(*a.cache, a.q, a.q_dtype, a.sm_scale * kLog2e, ep, ws);
   return PQB_OK;
 }
@@ -496,6 +560,17 @@ static int dispatch_dq_mn(const DecodeArgs& a, const EpiArgs& ep, const WorkSpli
                           bool& handled) {
   handled = true;
   const int mn = a.cache->angle_bits * 10 + a.cache->radius_bits;
+  if (a.cache->store.value_dtype == PQB_VQ4) {
+    switch (mn) {
+      case 44: return launch_dq<G, 4, 4, 0, 1>(a, ep, ws, grid, s);
+      case 32: return launch_dq<G, 3, 2, 0, 1>(a, ep, ws, grid, s);
+      case 22: return launch_dq<G, 2, 2, 0, 1>(a, ep, ws, grid, s);
+      case 42: return launch_dq<G, 4, 2, 0, 1>(a, ep, ws, grid, s);
+      case 24: return launch_dq<G, 2, 4, 0, 1>(a, ep, ws, grid, s);
+      case 34: return launch_dq<G, 3, 4, 0, 1>(a, ep, ws, grid, s);
+      default: handled = false; return PQB_OK;
+    }
+  }
   if (mn == 44 && (a.flags & PQB_DECODE_PROBE_MEM)) return launch_dq<G, 4, 4, 1>(a, ep, ws, grid, s);
   if (mn == 44 && (a.flags & PQB_DECODE_PROBE_COMPUTE)) return launch_dq<G, 4, 4, 2>(a, ep, ws, grid, s);
   switch (mn) {

@@ -615,6 +615,70 @@ __global__ void store_values_kernel(const void* __restrict__ vals, int src_dtype
   }
 }
 
+// PQB_VQ4 pages: _quantize_slices along each token row (baseline_quant.py:58-66:
+// zp = min, scale = fl(fl(max - zp) / 15), code = rint(fl(fl(v - zp) / scale))
+// clipped to [0, 15], scale == 0 -> 0), written in the fragment order of
+// vq4_pos().  One CTA per (32-token tile, unit); tile starts are 32-aligned.
+__global__ void __launch_bounds__(256) store_values_vq4_kernel(const void* __restrict__ vals, int src_dtype,
+                                                               int64_t T, int64_t unit_stride, int64_t tok_stride,
+                                                               pqb_store st, int64_t tok_offset_const,
+                                                               int32_t* __restrict__ flags) {
+  __shared__ uint8_t codes[32][132];
+  __shared__ float2 params[32];
+  const int64_t unit = blockIdx.y;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  bool bad = false;
+  for (int r = warp; r < 32; r += 8) {  // token rows: warp-wide min / max, then codes
+    const int64_t t = t0 + r;
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[k] = 0.0f;
+      if (vals && t < T) {
+        const int64_t so = unit * unit_stride + t * tok_stride + lane + 32 * k;
+        v[k] = src_dtype == PQB_F32 ? load1<PQB_F32>(vals, so)
+                                    : (src_dtype == PQB_BF16 ? load1<PQB_BF16>(vals, so) : load1<PQB_F16>(vals, so));
+      }
+      bad |= !(fabsf(v[k]) <= 3.40282347e38f);
+    }
+    float mn = fminf(fminf(v[0], v[1]), fminf(v[2], v[3])), mx = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    }
+    const float scale = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float raw = scale == 0.0f ? 0.0f : rintf(__fdiv_rn(__fsub_rn(v[k], mn), scale));
+      raw = fminf(fmaxf(raw, 0.0f), 15.0f);
+      codes[r][lane + 32 * k] = t < T ? static_cast<uint8_t>(raw) : 0;
+    }
+    if (lane == 0) params[r] = t < T ? make_float2(mn, scale) : make_float2(0.0f, 0.0f);
+  }
+  __syncthreads();
+  const int64_t ta = tok_offset_const + t0;
+  const int64_t page = ta / st.page_tokens;
+  const int64_t tp = ta - page * st.page_tokens;  // multiple of 32
+  uint8_t* pb = page_base(st, unit, page);
+  uint32_t* wout = reinterpret_cast<uint32_t*>(pb + st.value_off + (tp >> 5) * 2048);
+  for (int w = threadIdx.x; w < 512; w += blockDim.x) {
+    const int mt = w >> 6, ks = (w >> 5) & 1, ln = w & 31, g = ln >> 2, tq = ln & 3;
+    uint32_t word = 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int t = 16 * ks + 2 * tq + c + 8 * (k >> 1), e = 16 * mt + g + 8 * (k & 1);
+        word |= static_cast<uint32_t>(codes[t][e]) << (4 * k + 16 * c);
+      }
+    wout[w] = word;
+  }
+  if (threadIdx.x < 32) reinterpret_cast<float2*>(pb + vq4_params_off(st))[tp + threadIdx.x] = params[threadIdx.x];
+  if (bad && flags) atomicOr(flags, PQB_FLAG_NONFINITE);
+}
+
 __global__ void store_residual_kernel(const void* __restrict__ keys, int src_dtype, int64_t T, int d,
                                       int64_t unit_stride, int64_t tok_stride, float* __restrict__ ring,
                                       int res_cap, int64_t tok_offset_const, int32_t* __restrict__ flags) {
@@ -636,6 +700,51 @@ __global__ void store_residual_kernel(const void* __restrict__ keys, int src_dty
 }
 
 // ----------------------------------------------------------------- K5
+
+// One token's value row into a PQB_VQ4 page (append): quantize as
+// store_values_vq4_kernel, OR the nibbles into the tile's words (pages start
+// zeroed and every token slot is written once).  red: >= 2 * 32 floats of
+// shared scratch.  Caller: the whole block (d = 128 threads or more).
+__device__ void append_value_vq4(const pqb_cache& c, int64_t unit, int64_t T, const void* vals, int val_dtype,
+                                 float* red, bool& bad) {
+  const int e = threadIdx.x, lane = e & 31, warp = e >> 5, nw = (blockDim.x + 31) >> 5;
+  float v = 0.0f;
+  if (e < 128 && vals) {
+    const int64_t ko = unit * 128 + e;
+    v = val_dtype == PQB_F32 ? load1<PQB_F32>(vals, ko)
+                             : (val_dtype == PQB_BF16 ? load1<PQB_BF16>(vals, ko) : load1<PQB_F16>(vals, ko));
+  }
+  if (e < 128) bad |= !(fabsf(v) <= 3.40282347e38f);
+  float mn = e < 128 ? v : INFINITY, mx = e < 128 ? v : -INFINITY;
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if (lane == 0) {
+    red[warp] = mn;
+    red[32 + warp] = mx;
+  }
+  __syncthreads();
+  mn = INFINITY;
+  mx = -INFINITY;
+  for (int w = 0; w < nw; ++w) {
+    mn = fminf(mn, red[w]);
+    mx = fmaxf(mx, red[32 + w]);
+  }
+  const float scale = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
+  const int64_t page = T / c.store.page_tokens, tp = T - page * c.store.page_tokens;
+  uint8_t* pb = page_base(c.store, unit, page);
+  if (e < 128) {
+    float raw = scale == 0.0f ? 0.0f : rintf(__fdiv_rn(__fsub_rn(v, mn), scale));
+    raw = fminf(fmaxf(raw, 0.0f), 15.0f);
+    int w, sh;
+    vq4_pos(static_cast<int>(tp & 31), e, w, sh);
+    const uint32_t bits = static_cast<uint32_t>(raw) << sh;
+    if (bits) atomicOr(reinterpret_cast<unsigned int*>(pb + c.store.value_off + (tp >> 5) * 2048) + w, bits);
+  }
+  if (e == 0) reinterpret_cast<float2*>(pb + vq4_params_off(c.store))[tp] = make_float2(mn, scale);
+  __syncthreads();
+}
 
 // One block per unit.  kv_cache.py:179-189 with the residual deque as a ring.
 __global__ void __launch_bounds__(256) append_kernel(pqb_cache c, const void* __restrict__ keys, int key_dtype,
@@ -666,13 +775,14 @@ __global__ void __launch_bounds__(256) append_kernel(pqb_cache c, const void* __
                          clamps, bad);
   }
   __syncthreads();  // the flushed slot is read before it is overwritten
+  if (c.store.value_dtype == PQB_VQ4) append_value_vq4(c, unit, T, vals, val_dtype, s_scale + half, bad);
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
     const int64_t ko = unit * d + e;
     const float kv = key_dtype == PQB_F32 ? load1<PQB_F32>(keys, ko)
                                           : (key_dtype == PQB_BF16 ? load1<PQB_BF16>(keys, ko) : load1<PQB_F16>(keys, ko));
     bad |= !(fabsf(kv) <= 3.40282347e38f);
     if (c.res_cap > 0) c.residual[(unit * c.res_cap + T % c.res_cap) * d + e] = kv;
-    if (c.store.value_off >= 0) {
+    if (c.store.value_off >= 0 && c.store.value_dtype != PQB_VQ4) {
       float v = 0.0f;
       if (vals)
         v = val_dtype == PQB_F32 ? load1<PQB_F32>(vals, ko)
@@ -833,8 +943,14 @@ int launch_encode(const EncodeArgs& a, cudaStream_t s) {
 }
 
 int launch_store_values(const void* vals, int dtype, int64_t n_units, int64_t T, int d, int64_t us, int64_t ts,
-                        const pqb_store& st, const int32_t* tok_offset, int64_t tok_offset_const, cudaStream_t s) {
+                        const pqb_store& st, const int32_t* tok_offset, int64_t tok_offset_const, cudaStream_t s,
+                        int32_t* flags) {
   if (T == 0) return 0;
+  if (st.value_dtype == PQB_VQ4) {
+    dim3 grid(static_cast<unsigned>((T + 31) / 32), static_cast<unsigned>(n_units));
+    store_values_vq4_kernel<<<grid, 256, 0, s>>>(vals, dtype, T, us, ts, st, tok_offset_const, flags);
+    return 0;
+  }
   const int eb = dtype == PQB_F32 ? 4 : 2;
   const bool vec = d == 128 && st.value_dtype == PQB_BF16 && tok_offset == nullptr && st.value_off % 16 == 0 &&
                    st.page_bytes % 16 == 0 && (vals == nullptr || (reinterpret_cast<uintptr_t>(vals) % 16 == 0 &&
@@ -865,7 +981,7 @@ int launch_store_residual(const pqb_cache& c, const void* keys, int dtype, int64
 
 int launch_append(const pqb_cache& c, int64_t n_units, const void* keys, int key_dtype, const void* vals,
                   int val_dtype, unsigned long long* clamp_counts, int32_t* flags, cudaStream_t s) {
-  const size_t shm = sizeof(float) * (c.d / 2);
+  const size_t shm = sizeof(float) * (c.d / 2 + 64);
   append_kernel<<<static_cast<unsigned>(n_units), 128, shm, s>>>(c, keys, key_dtype, vals, val_dtype, clamp_counts,
                                                                   flags);
   return 0;

@@ -60,7 +60,8 @@ int launch_encode(const EncodeArgs& a, cudaStream_t s);
 // encode_fast.cu: persistent TMA-fed encoder for d = 128, m, n in {2,3,4}; false if the call does not qualify.
 bool launch_encode_fast(const EncodeArgs& a, cudaStream_t s);
 int launch_store_values(const void* vals, int dtype, int64_t n_units, int64_t T, int d, int64_t us, int64_t ts,
-                        const pqb_store& st, const int32_t* tok_offset, int64_t tok_offset_const, cudaStream_t s);
+                        const pqb_store& st, const int32_t* tok_offset, int64_t tok_offset_const, cudaStream_t s,
+                        int32_t* flags = nullptr);
 int launch_store_residual(const pqb_cache& c, const void* keys, int dtype, int64_t n_units, int64_t T, int64_t us,
                           int64_t ts, int64_t tok_offset_const, int32_t* flags, cudaStream_t s);
 int launch_append(const pqb_cache& c, int64_t n_units, const void* keys, int key_dtype, const void* vals,

@@ -111,9 +111,7 @@ __global__ void read_values_kernel(pqb_store st, int64_t unit, int d, int64_t T,
     const int64_t t = i / d;
     const int e = static_cast<int>(i - t * d);
     const int64_t page = t / P;
-    const uint8_t* vb = page_base_m(st, unit, page) + st.value_off + value_offset(t - page * P, e, d, st.value_dtype);
-    out[i] = st.value_dtype == PQB_F32 ? *reinterpret_cast<const float*>(vb)
-                                       : __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(vb));
+    out[i] = load_value(st, page_base_m(st, unit, page), t - page * P, e, d);
   }
 }
 

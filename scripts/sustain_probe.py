@@ -15,8 +15,10 @@ import bench
 from paper_2502_00527_b200 import _lib
 
 flags = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+vbits = int(sys.argv[2]) if len(sys.argv) > 2 else None  # 4: the 4-bit value mode
 dev = torch.device("cuda", 0)
-w = bench.DecodeWorkload(dev, layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, page_tokens=128, seed=0)
+w = bench.DecodeWorkload(dev, layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, page_tokens=128, seed=0,
+                         value_bits=vbits)
 algo = w.bytes_per_launch()
 run = w.capture(lambda: w.step(_lib.PQB_DECODE_NO_COMBINE | flags))
 Path("gpurun_out").mkdir(exist_ok=True)
@@ -37,4 +39,6 @@ for _ in range(3):
     ms = w.timed(run, 2, 0) / w.L
     idle_after.append(round(algo / (ms * 1e-3) / 1e9 / 6546.9, 3))
 smi.terminate()
-print(json.dumps({"flags": flags, "chunk_rates": rates, "after_2s_idle": idle_after}))
+step_ms = w.timed(w.capture(w.step), 10, 2)
+print(json.dumps({"flags": flags, "value_bits": vbits, "chunk_rates": rates, "after_2s_idle": idle_after,
+                  "tokens_per_s_cool": round(w.batch / (step_ms * 1e-3), 1)}))

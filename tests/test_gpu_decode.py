@@ -315,3 +315,86 @@ def test_dq_extreme_scales_and_zero_query():
         for g in range(G):
             ref = exact.lut_scores(q[u, g], a, r, s16, 4, 4, 1)
             peak_close(out[u, g], po.softmax64(ref, 1.0 / math.sqrt(128)) @ vb, OUT_RTOL_F32)
+
+
+# ---------------------------------------------------------------- 4-bit values
+
+
+def _vq4_cache(m, n, lay, res, lens, G, seed, shuffle=False):
+    U = len(lens)
+    T = max(lens)
+    keys = [po.synthetic_keys(t, 128, seed=seed + u, outliers=(0, 1), layout=lay) for u, t in enumerate(lens)]
+    rng = np.random.default_rng(seed)
+    vals = [rng.standard_normal((t, 128)).astype(np.float32) for t in lens]
+    for v in vals:  # constant rows (scale 0) and a wide one
+        v[min(3, len(v) - 1)] = 0.25
+        v[len(v) // 2] *= 50.0
+    q = rng.standard_normal((U, G, 128)).astype(np.float32)
+    cache = pq.PolarKVCache(pq.QuantConfig(m, n, LAY[lay]), U, 128, res, capacity=T + 8, value_bits=4,
+                            shuffle_pages=shuffle)
+    for u in range(U):
+        cache.prefill(torch.from_numpy(keys[u]).cuda().unsqueeze(0), torch.from_numpy(vals[u]).cuda().unsqueeze(0),
+                      unit_start=u)
+    return cache, keys, vals, q
+
+
+def _vq4_check(cache, keys, vals, q, m, n, lay, res, lens, outs, tol=OUT_RTOL_F32):
+    for u, t_u in enumerate(lens):
+        codes, zp, sc = po.quantize_values(vals[u], 4)
+        deq = po.dequantize_values(codes, zp, sc)
+        got = cache.values_f32(u).cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), deq.view(np.uint32))  # values() bit-identical
+        a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
+        s16 = cache.scales16[u].cpu().numpy()
+        resid = keys[u][t_u - min(res, t_u):] if res else np.zeros((0, 128), np.float32)
+        for g in range(q.shape[1]):
+            ref = po.lut_scores(q[u, g], a, r, s16, m, n, lay, resid)
+            o_ref = po.softmax64(ref, 1.0 / math.sqrt(128)) @ deq.astype(np.float64)
+            for out in outs:
+                peak_close(out[u, g], o_ref, tol)
+
+
+@pytest.mark.parametrize("m,n", [(4, 4), (3, 2), (2, 4)])
+@pytest.mark.parametrize("G", [4, 8])
+@pytest.mark.parametrize("lay,res", [(1, 0), (0, 40)])
+def test_vq4_decode_vs_oracle(m, n, G, lay, res):
+    """4-bit per-token values (PackedKVCache(quantize_values=True)) read inside
+    the DQ kernel: values() bit-identical to the reference quantizer (pinned by
+    tests/golden/golden_values.npz), fused output within the fp32 tolerance of
+    softmax64(LUT scores) . values(); the generic kernel agrees."""
+    lens = [3000, 1777, 33]
+    cache, keys, vals, q = _vq4_cache(m, n, lay, res, lens, G, seed=900 + 10 * m + n, shuffle=True)
+    qd = torch.from_numpy(q).cuda()
+    out = cache.decode(qd).cpu().numpy()
+    gen = cache.decode(qd, flags=pq._lib.PQB_DECODE_FORCE_GENERIC).cpu().numpy()
+    _vq4_check(cache, keys, vals, q, m, n, lay, res, lens, [out, gen])
+
+
+def test_vq4_append_and_bf16_out():
+    """Streaming append into 4-bit value pages (nibbles OR-ed into the tile
+    words), G = 1 (generic kernel) and bf16 output."""
+    lens = [500, 257]
+    m, n, lay, res = 4, 4, 1, 16
+    cache, keys, vals, q = _vq4_cache(m, n, lay, res, lens, 4, seed=77)
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        k_new = rng.standard_normal((2, 128)).astype(np.float32)
+        v_new = rng.standard_normal((2, 128)).astype(np.float32)
+        cache.append(torch.from_numpy(k_new).cuda(), torch.from_numpy(v_new).cuda())
+        for u in range(2):
+            keys[u] = np.concatenate([keys[u], k_new[u:u + 1]])
+            vals[u] = np.concatenate([vals[u], v_new[u:u + 1]])
+    lens = [len(v) for v in vals]
+    qd = torch.from_numpy(q).cuda()
+    out = cache.decode(qd).cpu().numpy()
+    out1 = np.stack([cache.decode(qd[:, g:g + 1]).cpu().numpy()[:, 0] for g in range(4)], axis=1)
+    _vq4_check(cache, keys, vals, q, m, n, lay, res, lens, [out, out1])
+    ob = cache.decode(qd, out_dtype=torch.bfloat16).float().cpu().numpy()
+    peak_close(ob, out, 2.0 ** -7)
+
+
+def test_vq4_rejects_other_widths():
+    with pytest.raises(ValueError):
+        pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 128, 0, value_bits=2)
+    with pytest.raises(ValueError):
+        pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 64, 0, value_bits=4)

@@ -115,3 +115,26 @@ def test_tables_match_reference(golden, m):
 def test_case_listing(golden):
     assert case_names(golden, "enc") == [f"enc{i}" for i in range(12)]
     assert case_names(golden, "cache") == [f"cache{i}" for i in range(6)]
+
+
+@pytest.fixture(scope="module")
+def golden_values():
+    from pathlib import Path
+
+    data = np.load(Path(__file__).resolve().parent / "golden" / "golden_values.npz")
+    return {k: data[k] for k in data.files}
+
+
+@pytest.mark.parametrize("idx", range(4))
+def test_value_quantizer_matches_reference(golden_values, idx):
+    """Per-token uniform value codes (the PackedKVCache quantize_values mode):
+    codes, zero points, scales and dequantized rows bit-identical to the
+    reference's quantize_uniform / dequantize_uniform / values()."""
+    g = {k.split("/", 1)[1]: v for k, v in golden_values.items() if k.startswith(f"v{idx}/")}
+    codes, zp, sc = po.quantize_values(g["values"], int(g["bits"]))
+    assert np.array_equal(codes, g["codes"])
+    assert np.array_equal(zp.view(np.uint32), g["zero_point"].view(np.uint32))
+    assert np.array_equal(sc.view(np.uint32), g["scale"].view(np.uint32))
+    deq = po.dequantize_values(codes, zp, sc)
+    assert np.array_equal(deq.view(np.uint32), g["dequant"].view(np.uint32))
+    assert np.array_equal(deq.view(np.uint32), g["cache_values"].view(np.uint32))
