@@ -135,6 +135,59 @@ __global__ void __launch_bounds__(256) radius_max_v8_kernel(const void* __restri
   }
 }
 
+// Threshold seed for the dense pass: the exact max of d2 over every 64th token
+// row of each unit (1/64 of the bytes), atomically max-ed into maxsq.  The
+// dense pass starts its candidate thresholds at fl32(seed) * (1 - 2^-20)
+// instead of 0: an element whose d2 can reach the final max has
+// f >= d2 (1 - 2^-23) >= seed (1 - 2^-23) > that threshold, so exactness is
+// unchanged, while the early-row candidate flood (at warp level, nearly
+// every iteration took the double-precision branch) disappears.
+constexpr int kSeedStride = 64;
+
+template <int DT, int LAYOUT>
+__global__ void __launch_bounds__(256) radius_seed_kernel(const void* __restrict__ keys, int64_t T, int half,
+                                                          int64_t unit_stride, unsigned long long* __restrict__ maxsq) {
+  const int unit = blockIdx.y;
+  const int tpr = half >> 3;
+  const int rows = 256 / tpr;
+  const int cg = threadIdx.x % tpr, row = threadIdx.x / tpr;
+  unsigned long long dmax[8] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+  const int64_t n_samples = (T + kSeedStride - 1) / kSeedStride;
+  for (int64_t s = static_cast<int64_t>(blockIdx.x) * rows + row; s < n_samples; s += static_cast<int64_t>(gridDim.x) * rows) {
+    const int64_t rb = static_cast<int64_t>(unit) * unit_stride + s * kSeedStride * 2 * half;
+    float x[8], y[8];
+    if constexpr (LAYOUT == PQB_HALF_SPLIT) {
+      load8<DT>(keys, rb + 8 * cg, x);
+      load8<DT>(keys, rb + half + 8 * cg, y);
+    } else {
+      float v0[8], v1[8];
+      load8<DT>(keys, rb + 16 * cg, v0);
+      load8<DT>(keys, rb + 16 * cg + 8, v1);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        x[i] = v0[2 * i]; y[i] = v0[2 * i + 1];
+        x[4 + i] = v1[2 * i]; y[4 + i] = v1[2 * i + 1];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double xd = x[i], yd = y[i];
+      const unsigned long long db = dbits(__fma_rn(xd, xd, __dmul_rn(yd, yd)));
+      dmax[i] = db > dmax[i] ? db : dmax[i];
+    }
+  }
+  __shared__ unsigned long long s_red[8][256];  // block max first: one atomic per (block, channel)
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s_red[i][threadIdx.x] = dmax[i];
+  __syncthreads();
+  for (int c = threadIdx.x; c < half; c += 256) {
+    const int g = c >> 3, i = c & 7;
+    unsigned long long m = 0ull;
+    for (int r = 0; r < rows; ++r) m = s_red[i][r * tpr + g] > m ? s_red[i][r * tpr + g] : m;
+    if (m) atomicMax(maxsq + static_cast<int64_t>(unit) * half + c, m);
+  }
+}
+
 // Same reduction for dense rows (tok_stride == d) fed by the TMA bulk-copy
 // engine: a 4-stage ring of 16 KB row blocks per CTA keeps ~64 KB per CTA in
 // flight independent of register pressure; threads read their 8-channel
@@ -178,9 +231,12 @@ __global__ void __launch_bounds__(256) radius_max_tma_kernel(const void* __restr
   unsigned long long dmax[8];
   uint32_t thr[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < 8; ++i) {  // seeded by radius_seed_kernel (exact d2 of sampled rows)
     dmax[i] = 0ull;
-    thr[i] = 0u;
+    const double seed = __longlong_as_double(static_cast<long long>(
+        __ldcg(maxsq + static_cast<int64_t>(unit) * half + 8 * cg + i)));
+    const float sf = __double2float_rd(seed) * (1.0f - 0x1p-20f);
+    thr[i] = sf <= 3.40282347e38f ? __float_as_uint(sf) : 0u;  // NaN / Inf seed: every element a candidate
   }
   for (int k = 0; k < n_stages; ++k) {
     const int slot = k % kRmaxStages;
@@ -836,6 +892,17 @@ int launch_radius_scales(const RadiusScalesArgs& a, cudaStream_t s) {
                      kRmaxStageBytes % (a.d * eb) == 0 && (a.unit_stride * eb) % 16 == 0;
   if (dense) {
     const size_t shm = kRmaxStages * kRmaxStageBytes;
+    const int64_t n_samples = (a.tokens + kSeedStride - 1) / kSeedStride;
+    dim3 sgrid(static_cast<unsigned>(std::min<int64_t>((n_samples * (a.d / 16) + 255) / 256, 8)),
+               static_cast<unsigned>(a.n_units));
+    switch (a.key_dtype * 2 + a.layout) {
+      case PQB_F32 * 2 + PQB_ADJACENT: radius_seed_kernel<PQB_F32, PQB_ADJACENT><<<sgrid, 256, 0, s>>>(a.keys, a.tokens, a.d / 2, a.unit_stride, a.maxsq_ws); break;
+      case PQB_F32 * 2 + PQB_HALF_SPLIT: radius_seed_kernel<PQB_F32, PQB_HALF_SPLIT><<<sgrid, 256, 0, s>>>(a.keys, a.tokens, a.d / 2, a.unit_stride, a.maxsq_ws); break;
+      case PQB_BF16 * 2 + PQB_ADJACENT: radius_seed_kernel<PQB_BF16, PQB_ADJACENT><<<sgrid, 256, 0, s>>>(a.keys, a.tokens, a.d / 2, a.unit_stride, a.maxsq_ws); break;
+      case PQB_BF16 * 2 + PQB_HALF_SPLIT: radius_seed_kernel<PQB_BF16, PQB_HALF_SPLIT><<<sgrid, 256, 0, s>>>(a.keys, a.tokens, a.d / 2, a.unit_stride, a.maxsq_ws); break;
+      case PQB_F16 * 2 + PQB_ADJACENT: radius_seed_kernel<PQB_F16, PQB_ADJACENT><<<sgrid, 256, 0, s>>>(a.keys, a.tokens, a.d / 2, a.unit_stride, a.maxsq_ws); break;
+      default: radius_seed_kernel<PQB_F16, PQB_HALF_SPLIT><<<sgrid, 256, 0, s>>>(a.keys, a.tokens, a.d / 2, a.unit_stride, a.maxsq_ws); break;
+    }
     switch (a.key_dtype * 2 + a.layout) {
       case PQB_F32 * 2 + PQB_ADJACENT: launch_rmax_tma<PQB_F32, PQB_ADJACENT>(a, chunk, grid, shm, s); break;
       case PQB_F32 * 2 + PQB_HALF_SPLIT: launch_rmax_tma<PQB_F32, PQB_HALF_SPLIT>(a, chunk, grid, shm, s); break;

@@ -34,7 +34,10 @@ namespace pqb {
 
 namespace {
 
-constexpr int kEfWarps = 16;     // warps per CTA (one CTA per SM)
+#ifndef PQB_EF_WARPS
+#define PQB_EF_WARPS 16
+#endif
+constexpr int kEfWarps = PQB_EF_WARPS;  // warps per CTA (one CTA per SM)
 constexpr int kEfStages = 3;     // ring depth per warp
 constexpr int kEfItemTok = 512;  // tokens per work item (one unit)
 constexpr int kEfAlign = 16;     // start token / page alignment the kernel needs
