@@ -231,6 +231,12 @@ __global__ void __launch_bounds__(kNW * 32, 1)
                                                 __float2half_rn(static_cast<float>(y - __half2float(yh))))));
   }
   const uint32_t ptab_l = smem_u32(smem) + ((lane & 15) << 3);  // this lane's bank-slot copy
+  // Programmatic dependent launch: everything above uses constants only; the
+  // cache, q and the outputs may belong to the previous kernel in the stream.
+  // Let the next launch start its own prologue as SMs drain, then wait for
+  // this grid's predecessors to complete.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tpp = c.store.page_tokens / kTile;  // tiles per page
   const int64_t i_begin = static_cast<int64_t>(blockIdx.x) * ws.per_cta;
   const int64_t i_end = min(ws.items, i_begin + ws.per_cta);
@@ -550,8 +556,21 @@ static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws
     }
     attr_set = true;
   }
-  decode_dq_kernel<G, M, N, PROBE, VQ>
-      <<<grid, kNW * 32, Cfg::kSmem, s>>>(*a.cache, a.q, a.q_dtype, a.sm_scale * kLog2e, ep, ws);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kNW * 32);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, decode_dq_kernel<G, M, N, PROBE, VQ>, *a.cache, a.q, a.q_dtype,
+                         a.sm_scale * kLog2e, ep, ws) != cudaSuccess) {
+    set_error("decode_dq launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return PQB_ECUDA;
+  }
   return PQB_OK;
 }
 
