@@ -167,20 +167,39 @@ struct WorkSplit {
 PQB_DEV int64_t first_cta(const WorkSplit& w, int64_t unit) { return (unit * w.tiles_max) / w.per_cta; }
 PQB_DEV int64_t last_cta(const WorkSplit& w, int64_t unit) { return ((unit + 1) * w.tiles_max - 1) / w.per_cta; }
 
-// LSE merge of a unit's segment partials: out = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M)
+// LSE merge of a unit's segment partials: out = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
+// It runs in the tail of the launch (the last CTA of a unit), so its L2 reads
+// are issued together: up to 8 segments in one batch of independent loads.
 PQB_DEV void merge_slots(const EpiArgs& ep, int64_t unit, int nseg, int G, int tid, int nthreads) {
+  constexpr int kB = 8;
   for (int i = tid; i < G * 128; i += nthreads) {
     const int g = i >> 7, e = i & 127;
-    float mx = -INFINITY;
-    for (int s = 0; s < nseg; ++s) mx = fmaxf(mx, __ldcg(ep.part_ml + 2 * ((unit * ep.slots + s) * G + g)));
-    float L = 0.0f, O = 0.0f;
-    for (int s = 0; s < nseg; ++s) {
-      const int64_t sl = (unit * ep.slots + s) * G + g;
-      const float ms = __ldcg(ep.part_ml + 2 * sl);
-      if (ms == -INFINITY) continue;
-      const float sc = exp2f(ms - mx);
-      L = fmaf(__ldcg(ep.part_ml + 2 * sl + 1), sc, L);
-      O = fmaf(__ldcg(ep.part_o + sl * 128 + e), sc, O);
+    float mx = -INFINITY, L = 0.0f, O = 0.0f;
+    for (int s0 = 0; s0 < nseg; s0 += kB) {
+      float ms[kB], ls[kB], os[kB];
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        const int64_t sl = (unit * ep.slots + s0 + k) * G + g;
+        const bool ok = s0 + k < nseg;
+        ms[k] = ok ? __ldcg(ep.part_ml + 2 * sl) : -INFINITY;
+        ls[k] = ok ? __ldcg(ep.part_ml + 2 * sl + 1) : 0.0f;
+        os[k] = ok ? __ldcg(ep.part_o + sl * 128 + e) : 0.0f;
+      }
+      float bm = mx;
+#pragma unroll
+      for (int k = 0; k < kB; ++k) bm = fmaxf(bm, ms[k]);
+      if (bm == -INFINITY) continue;
+      const float r = exp2f(mx - bm);  // rescale what was merged so far (0 when mx = -inf)
+      L *= r;
+      O *= r;
+#pragma unroll
+      for (int k = 0; k < kB; ++k) {
+        if (ms[k] == -INFINITY) continue;
+        const float sc = exp2f(ms[k] - bm);
+        L = fmaf(ls[k], sc, L);
+        O = fmaf(os[k], sc, O);
+      }
+      mx = bm;
     }
     store_out(ep.out, ep.out_dtype, (unit * G + g) * 128 + e, O / L);
   }
