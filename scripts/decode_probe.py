@@ -1,0 +1,19 @@
+"""Small driver for ncu: a few configs[1]-shaped decode steps (128 units x 32K
+tokens per layer, m4n4, G=4); argv[1] = value bits (0: bf16 values, 4: the
+4-bit value mode), argv[2] = layers."""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch
+
+import bench
+
+vb = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+L = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+w = bench.DecodeWorkload(torch.device("cuda", 0), layers=L, batch=16, hq=32, hkv=8, T=32768, m=4, n=4,
+                         page_tokens=128, seed=0, value_bits=vb or None)
+for _ in range(3):
+    w.step()
+torch.cuda.synchronize()
+print("ok")
