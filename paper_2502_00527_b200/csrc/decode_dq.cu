@@ -175,19 +175,44 @@ PQB_DEV uint2 lds_u2(uint32_t addr) {
 // and the zero points join as sum_t p_t zp_t per query:
 //   o = sum_t p_t (c_t s_t + z_t) = [codes] . (p s) + sum_t p_t z_t.
 template <int M, int N, int VQ>
-PQB_DEV void issue_tile_dq(uint8_t* st, const pqb_store& s, const uint8_t* pb, int tile, int tpp, uint64_t* bar) {
+PQB_DEV void issue_tile_dq(uint8_t* st, const pqb_store& s, const uint8_t* pb, int tin, uint64_t* bar) {
+  // tin: tile index within the page (tokens tin * 32 ...)
+  constexpr uint32_t kA = kTile * 8 * M, kR = kTile * 8 * N;
+  const int in_page = tin * kTile;
   if constexpr (!VQ) {
-    issue_tile<M, N>(st, s, pb, tile, tpp, true, bar);
+    constexpr uint32_t kV = kTile * 256;
+    mbar_arrive_expect_tx(bar, kA + kR + kV);
+    bulk_g2s(st, pb + s.angle_off + in_page * 8 * M, kA, bar);
+    bulk_g2s(st + kA, pb + s.radius_off + in_page * 8 * N, kR, bar);
+    bulk_g2s(st + kA + kR, pb + s.value_off + in_page * 256, kV, bar);
   } else {
-    constexpr uint32_t kA = kTile * 8 * M, kR = kTile * 8 * N;
-    const int tin = tile % tpp, in_page = tin * kTile;
     mbar_arrive_expect_tx(bar, kA + kR + 2048 + kTile * 8);
     bulk_g2s(st, pb + s.angle_off + in_page * 8 * M, kA, bar);
     bulk_g2s(st + kA, pb + s.radius_off + in_page * 8 * N, kR, bar);
-    bulk_g2s(st + kA + kR, pb + s.value_off + static_cast<int64_t>(tin) * 2048, 2048, bar);
-    bulk_g2s(st + kA + kR + 2048, pb + vq4_params_off(s) + static_cast<int64_t>(in_page) * 8, kTile * 8, bar);
+    bulk_g2s(st + kA + kR, pb + s.value_off + tin * 2048, 2048, bar);
+    bulk_g2s(st + kA + kR + 2048, pb + vq4_params_off(s) + in_page * 8, kTile * 8, bar);
   }
 }
+
+// Lane 0's cursor over this warp's tiles (first, first + kNW, ...): page and
+// tile-in-page advanced incrementally (a division per segment, not per tile).
+struct TileCursor {
+  int tile, pg, tin;
+  PQB_DEV void init(int t, int tpp) {
+    tile = t;
+    pg = t / tpp;
+    tin = t - pg * tpp;
+  }
+  PQB_DEV void next(int dpg, int dtin, int tpp) {
+    tile += kNW;
+    pg += dpg;
+    tin += dtin;
+    if (tin >= tpp) {
+      tin -= tpp;
+      ++pg;
+    }
+  }
+};
 
 template <int G, int M, int N, int PROBE = 0, int VQ = 0>
 __global__ void __launch_bounds__(kNW * 32, 1)
@@ -238,6 +263,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int tpp = c.store.page_tokens / kTile;  // tiles per page
+  const int dpg = kNW / tpp, dtin = kNW - (kNW / tpp) * tpp;  // cursor step of kNW tiles
   const int64_t i_begin = static_cast<int64_t>(blockIdx.x) * ws.per_cta;
   const int64_t i_end = min(ws.items, i_begin + ws.per_cta);
   uint32_t k_iter = 0;
@@ -309,17 +335,19 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     const float xscale = ldexpf(sm_scale_log2, -e_sc);
 
     // ---- lane 0 fills this warp's ring with its first tiles
+    TileCursor cur;
+    cur.init(first, tpp);
     if (lane == 0) {
 #pragma unroll
       for (int s = 0; s < kStages; ++s) {
-        const int tile = first + s * kNW;
-        if (tile < t_hi) {
+        if (cur.tile < t_hi) {
           fence_proxy_async_smem();
           const uint32_t sl = (k_iter + s) % kStages;
           issue_tile_dq<M, N, VQ>(my_area + sl * Cfg::kStageBytes, c.store,
-                                  page_base_c(c.store, unit, PROBE == 2 ? 0 : tile / tpp), PROBE == 2 ? 0 : tile, tpp,
+                                  page_base_c(c.store, unit, PROBE == 2 ? 0 : cur.pg), PROBE == 2 ? 0 : cur.tin,
                                   bar + sl);
         }
+        cur.next(dpg, dtin, tpp);
       }
     }
     float m_run = -INFINITY, l_run = 0.0f;  // query g8 (lanes g8 < G)
@@ -338,10 +366,13 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       const int tok0 = tile * kTile;
       if constexpr (PROBE == 1) {
         __syncwarp();
-        if (lane == 0 && nt < t_hi) {
-          fence_proxy_async_smem();
-          issue_tile_dq<M, N, VQ>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, nt / tpp), nt,
-                                  tpp, bar + s);
+        if (lane == 0) {
+          if (nt < t_hi) {
+            fence_proxy_async_smem();
+            issue_tile_dq<M, N, VQ>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, cur.pg), cur.tin,
+                                    bar + s);
+          }
+          cur.next(dpg, dtin, tpp);
         }
         continue;
       }
@@ -490,11 +521,14 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         }
       }
       __syncwarp();
-      if (lane == 0 && nt < t_hi) {
-        fence_proxy_async_smem();
-        issue_tile_dq<M, N, VQ>(my_area + s * Cfg::kStageBytes, c.store,
-                                page_base_c(c.store, unit, PROBE == 2 ? 0 : nt / tpp), PROBE == 2 ? 0 : nt, tpp,
-                                bar + s);
+      if (lane == 0) {
+        if (nt < t_hi) {
+          fence_proxy_async_smem();
+          issue_tile_dq<M, N, VQ>(my_area + s * Cfg::kStageBytes, c.store,
+                                  page_base_c(c.store, unit, PROBE == 2 ? 0 : cur.pg), PROBE == 2 ? 0 : cur.tin,
+                                  bar + s);
+        }
+        cur.next(dpg, dtin, tpp);
       }
     }
 
