@@ -181,6 +181,22 @@ PQB_DEV void ef_radius2(F2 x, F2 y, F2 inv, float& rq0, float& rq1, float& worst
   rq1 = rq.y;
 }
 
+// Does pair (x, y) sit in an ambiguity band (or outside the safe magnitude
+// range)?  Exactly the fast path's arithmetic (FFMA2 / FMUL2 lanes are IEEE
+// single operations), so it flags the same pairs the combined metric did.
+template <int M>
+PQB_DEV bool ef_pair_flag(float x, float y, float inv, const uint8_t* tab) {
+  const float r2 = fmaf(x, x, y * y);
+  const bool rok = in_safe_range_nonneg(r2);
+  const float q = (r2 * rsqrt_approx(r2)) * inv;
+  const float rq = rintf(q);
+  const float dq = fmaf(rq, -1.0f, q);
+  const float m = fmaf(dq, dq, fmaf(q, 0x1p-18f, -0.25f));
+  float w = -1.0f;
+  (void)ef_angle<M>(x, y, w, tab);
+  return !rok || !(fmaxf(w, m) < 0.0f);
+}
+
 // Word w (0 <= w < 2B) of a token row of B-bit codes when lane-in-row j holds
 // codes 8j .. 8j+7 as chunk c (8B bits).  Shuffles stay inside the row's 8 lanes.
 template <int B>
@@ -390,9 +406,11 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
       const int row = 4 * it + r;
       const bool valid = row < rows;
       uint32_t ca = 0u, cr = 0u;
+      float x[8], y[8], rq[8];
+      uint32_t ac[8];
+      bool need = false;
       if (valid) {
         const uint8_t* rp = ring + slot * Cfg::kStageBytes + row * Cfg::kRowBytes;
-        float x[8], y[8];
         if constexpr (LAYOUT == PQB_HALF_SPLIT) {
           load8s<DT>(rp, 8 * cg, x);
           load8s<DT>(rp, 64 + 8 * cg, y);
@@ -406,8 +424,6 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
             x[4 + i] = v1[2 * i]; y[4 + i] = v1[2 * i + 1];
           }
         }
-        uint32_t ac[8];
-        float rq[8];
         float worst = -1.0f, worst_r = -1.0f;
         bool rok = true;
 #pragma unroll
@@ -416,19 +432,26 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
           ac[i] = ef_angle<M>(x[i], y[i], worst, octant_tab);
           ac[i + 1] = ef_angle<M>(x[i + 1], y[i + 1], worst, octant_tab);
         }
-        if (!(fmaxf(worst, worst_r) < 0.0f) || !rok) {
-          // rare: the exact pipeline for this lane's eight pairs (zero-scale
-          // channels are masked in ef_pack and need no exact work)
+        need = !(fmaxf(worst, worst_r) < 0.0f) || !rok;
+        if (!need) ef_pack<M, N>(ac, rq, keep_a, keep_r, clamps, ca, cr);
+      }
+      if (__any_sync(0xffffffffu, need)) {
+        // rare (~2% of warp iterations): the exact double-precision pipeline,
+        // per pair slot, only for slots some lane flagged (the flags are the
+        // fast path's own metrics recomputed bit-identically); zero-scale
+        // channels are masked in ef_pack and need no exact work
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (s32[i] > 0.0f) {
+        for (int i = 0; i < 8; ++i) {
+          const bool f = need && ef_pair_flag<M>(x[i], y[i], inv[i], octant_tab);
+          if (__any_sync(0xffffffffu, f)) {
+            if (f && s32[i] > 0.0f) {
               bad |= !(fabsf(x[i]) <= 3.40282347e38f && fabsf(y[i]) <= 3.40282347e38f);
               rq[i] = radius_raw_exact(x[i], y[i], s32[i]);
               ac[i] = angle_code_exact(x[i], y[i], M);
             }
           }
         }
-        ef_pack<M, N>(ac, rq, keep_a, keep_r, clamps, ca, cr);
+        if (need) ef_pack<M, N>(ac, rq, keep_a, keep_r, clamps, ca, cr);
       }
       // ---- the row's 2M angle words and 2N radius words (a stage never
       // straddles a page).  Row-word shuffles run on all lanes.
