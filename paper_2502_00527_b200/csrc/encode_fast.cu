@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
   const int64_t W = static_cast<int64_t>(gridDim.x) * kEfWarps;
   const int64_t gw = static_cast<int64_t>(blockIdx.x) * kEfWarps + warp;
   const int64_t my_items = p.items > gw ? (p.items - gw + W - 1) / W : 0;
-  const int64_t n_stage = my_items * kStagesPerItem;
+  const int n_stage = static_cast<int>(my_items * kStagesPerItem);  // < 2^31 stages per warp
   if (lane == 0) {
     for (int s = 0; s < kEfStages; ++s) mbar_init(bars + s, 1);
     fence_mbar_init();
@@ -323,9 +323,9 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
   };
   Cursor pc{gw, 0, 0, 0};  // producer (lane 0)
   cursor_item(pc);
-  int64_t p_g = 0;
+  int p_slot = 0;  // ring slot of the next issue (counters, not divisions: 3 stages)
   auto issue_next = [&]() {
-    const int slot = static_cast<int>(p_g % kEfStages);
+    const int slot = p_slot;
     const int rows = stage_rows(pc);
     if (rows == 0) {
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bars + slot)) : "memory");
@@ -337,11 +337,11 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
                                static_cast<int64_t>(DType<DT>::kBytes);
       bulk_g2s(ring + slot * Cfg::kStageBytes, src, bytes, bars + slot);
     }
-    ++p_g;
+    p_slot = p_slot + 1 == kEfStages ? 0 : p_slot + 1;
     cursor_next(pc);
   };
   if (lane == 0)
-    for (int64_t g = 0; g < kEfStages && g < n_stage; ++g) issue_next();
+    for (int g = 0; g < kEfStages && g < n_stage; ++g) issue_next();
 
   int64_t cur_unit = -1;
   float s32[8], inv[8];
@@ -362,7 +362,9 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
   cursor_item(cc);
   int64_t pg = 0;  // page of the stage's first token, and its row in the page
   int in_pg0 = 0;
-  for (int64_t g = 0; g < n_stage; ++g, cursor_next(cc)) {
+  int slot = 0;
+  uint32_t phase = 0;
+  for (int g = 0; g < n_stage; ++g, cursor_next(cc)) {
     const int64_t unit = cc.unit, t0 = cc.t_item + cc.st * kStageTok;
     const int rows = stage_rows(cc);
     if (cc.st == 0) {
@@ -396,8 +398,7 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
         }
       }
     }
-    const int slot = static_cast<int>(g % kEfStages);
-    mbar_wait(bars + slot, static_cast<uint32_t>((g / kEfStages) & 1));
+    mbar_wait(bars + slot, phase);
     const int64_t pid = p.st.page_table ? static_cast<int64_t>(__ldg(p.st.page_table + unit * p.st.max_pages + pg))
                                         : unit * p.st.max_pages + pg;
     uint8_t* pb = p.st.pool + pid * p.st.page_bytes;
@@ -466,6 +467,10 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
     if (lane == 0 && g + kEfStages < n_stage) {
       fence_proxy_async_smem();
       issue_next();
+    }
+    if (++slot == kEfStages) {
+      slot = 0;
+      phase ^= 1u;
     }
   }
   flush_clamps();
