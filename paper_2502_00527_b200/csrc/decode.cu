@@ -52,7 +52,7 @@ struct FastCfg {
   static constexpr int kStageBytes = kABytes + kRBytes + kVBytes;
   static constexpr int kPBytes = 2 * 8 * kTile * 2;  // bf16 [hi/lo][8 queries][32 tokens]
   static constexpr int kHeadBytes = (kLutFloats + kRtabFloats + G * 128 + 64) * 4;
-  static constexpr int kWarpBytes = kStages * kStageBytes + kPBytes + 64;
+  static constexpr int kWarpBytes = kStages * kStageBytes + kPBytes;
   static constexpr int kSmem = kHeadBytes + kNW * kWarpBytes + 128;
   static_assert(kHeadBytes % 16 == 0 && kWarpBytes % 16 == 0, "alignment");
   static_assert(kNW * kStages * kStageBytes >= kNW * G * 132 * 4, "merge area");
@@ -77,7 +77,11 @@ __global__ void __launch_bounds__(kNW * 32, 1)
   const bool want_out = ep.out != nullptr;
   uint8_t* my_area = warp_area + warp * Cfg::kWarpBytes;
   uint8_t* pbuf = my_area + kStages * Cfg::kStageBytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(pbuf + Cfg::kPBytes);
+  // mbarriers live outside the warp areas: the end-of-segment merge scratch
+  // (red, G * 132 floats per warp) aliases the stage memory and, at G = 8,
+  // would run over warp 0's barriers if they sat behind its stages
+  __shared__ uint64_t s_bar[kNW][kStages];
+  uint64_t* bar = s_bar[warp];
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(bar + s, 1);

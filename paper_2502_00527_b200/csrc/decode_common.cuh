@@ -178,12 +178,14 @@ PQB_DEV void merge_slots(const EpiArgs& ep, int64_t unit, int nseg, int G, int t
     for (int s0 = 0; s0 < nseg; s0 += kB) {
       float ms[kB], ls[kB], os[kB];
 #pragma unroll
-      for (int k = 0; k < kB; ++k) {
-        const int64_t sl = (unit * ep.slots + s0 + k) * G + g;
+      for (int k = 0; k < kB; ++k) {  // slots past nseg re-read the last one (in bounds) and are masked
         const bool ok = s0 + k < nseg;
-        ms[k] = ok ? __ldcg(ep.part_ml + 2 * sl) : -INFINITY;
-        ls[k] = ok ? __ldcg(ep.part_ml + 2 * sl + 1) : 0.0f;
-        os[k] = ok ? __ldcg(ep.part_o + sl * 128 + e) : 0.0f;
+        const int64_t sl = (unit * ep.slots + min(s0 + k, nseg - 1)) * G + g;
+        const float m = __ldcg(ep.part_ml + 2 * sl), l = __ldcg(ep.part_ml + 2 * sl + 1);
+        const float o = __ldcg(ep.part_o + sl * 128 + e);
+        ms[k] = ok ? m : -INFINITY;
+        ls[k] = ok ? l : 0.0f;
+        os[k] = ok ? o : 0.0f;
       }
       float bm = mx;
 #pragma unroll

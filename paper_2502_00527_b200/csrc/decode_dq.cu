@@ -60,7 +60,7 @@ struct DqCfg {
   static constexpr int kTabBytes = 128 << (M + N);          // product table, 16 bank-slot copies
   static constexpr int kFragBytes = 16 * 32 * 16;            // Q' A-fragments [ks][lane] uint4 (hi, lo, hi, lo)
   static constexpr int kHeadBytes = kTabBytes + kFragBytes + G * 128 * 4 + 128 + 8 * (1 << M);
-  static constexpr int kWarpBytes = kStages * kStageBytes + kPBytes + 64;
+  static constexpr int kWarpBytes = kStages * kStageBytes + kPBytes;
   static constexpr int kSmem = kHeadBytes + kNW * kWarpBytes + 128;
   static constexpr bool kPacked = G <= 4;  // P.V: columns 0-3 carry P_hi, 4-7 P_lo
   static_assert(kHeadBytes % 16 == 0 && kWarpBytes % 16 == 0, "alignment");
@@ -233,7 +233,11 @@ __global__ void __launch_bounds__(kNW * 32, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint8_t* my_area = warp_area + warp * Cfg::kWarpBytes;
   float* rbuf = reinterpret_cast<float*>(my_area + kStages * Cfg::kStageBytes);  // [32][8]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(my_area + kStages * Cfg::kStageBytes + Cfg::kPBytes);
+  // mbarriers live outside the warp areas: the end-of-segment merge scratch
+  // (red, G * 132 floats per warp) aliases the stage memory and, at G = 8,
+  // would run over warp 0's barriers if they sat behind its stages
+  __shared__ uint64_t s_bar[kNW][kStages];
+  uint64_t* bar = s_bar[warp];
   if (lane == 0) {
 #pragma unroll
     for (int s = 0; s < kStages; ++s) mbar_init(bar + s, 1);

@@ -398,3 +398,36 @@ def test_vq4_rejects_other_widths():
         pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 128, 0, value_bits=2)
     with pytest.raises(ValueError):
         pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 64, 0, value_bits=4)
+
+
+@pytest.mark.parametrize("page_tokens", [32, 64, 256, 512])
+@pytest.mark.parametrize("G", [4, 8])
+def test_dq_page_sizes(page_tokens, G):
+    """The decode kernel's per-warp tile cursor (page, tile-in-page advanced by
+    8 tiles per step) for 1, 2, 8 and 16 tiles per page, shuffled page tables,
+    ragged lengths that end mid-page."""
+    lens = [5000, 1057, 70]
+    U = len(lens)
+    keys = [po.synthetic_keys(t, 128, seed=40 + u, outliers=(0, 1)) for u, t in enumerate(lens)]
+    rng = np.random.default_rng(page_tokens + G)
+    vals = [rng.standard_normal((t, 128)).astype(np.float32) for t in lens]
+    q = rng.standard_normal((U, G, 128)).astype(np.float32)
+    cache = pq.PolarKVCache(pq.QuantConfig(4, 4), U, 128, 0, capacity=max(lens) + 1, page_tokens=page_tokens,
+                            shuffle_pages=True)
+    for u in range(U):
+        cache.prefill(torch.from_numpy(keys[u]).cuda().unsqueeze(0), torch.from_numpy(vals[u]).cuda().unsqueeze(0),
+                      unit_start=u)
+    qd = torch.from_numpy(q).cuda()
+    out = cache.decode(qd).cpu().numpy()
+    # regression: at G = 8 the end-of-segment merge scratch once overran warp
+    # 0's mbarriers (CTAs whose later segments issue TMA: the short third unit)
+    lut = cache.decode(qd, flags=pq._lib.PQB_DECODE_LUT).cpu().numpy()
+    for u in range(U):
+        a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
+        s16 = cache.scales16[u].cpu().numpy()
+        vb = torch.from_numpy(vals[u]).to(torch.bfloat16).float().numpy().astype(np.float64)
+        for g in range(G):
+            ref = po.lut_scores(q[u, g], a, r, s16, 4, 4, 1, np.zeros((0, 128), np.float32))
+            o_ref = po.softmax64(ref, 1.0 / math.sqrt(128)) @ vb
+            peak_close(out[u, g], o_ref, OUT_RTOL_F32)
+            peak_close(lut[u, g], o_ref, OUT_RTOL_F32)
