@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip configs 1/3/4/5 side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--sustain-seconds", type=float, default=2.5,
+                    help="extra back-to-back decode after the timed region, reported as 'sustained' (0: skip)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no timing claims)")
     ap.add_argument("--variant", choices=["auto", "lut", "dq"], default="auto",
                     help="scoring kernel of the fused decode (auto: the library's per-G choice)")
@@ -359,6 +361,25 @@ def run_ours(a, rank: int, world: int, dist) -> dict | None:
         o_host.copy_(w.out, non_blocking=True)
 
     ms_e2e = w.timed(e2e_step, max(3, a.steps // 2), 2, dist)
+
+    # ---- sustained: the same graph step back to back for a few seconds (the
+    #      board reaches its 1000 W cap within ~0.3 s; profiles/r01/power_probe.md);
+    #      reported beside the K-step value, not instead of it
+    sustained = None
+    if a.sustain_seconds > 0 and not a.no_graph:
+        import time as _t
+
+        with ClockSampler(dev) as sclk:
+            t_end = _t.time() + a.sustain_seconds
+            chunks = []
+            while _t.time() < t_end:
+                chunks.append(w.timed(run, 8, 0))
+        tail = chunks[len(chunks) // 2:] or chunks
+        ms_sus = sum(tail) / len(tail)
+        sustained = {"seconds": a.sustain_seconds, "ms_per_step": ms_sus,
+                     "value": (a.batch * world if a.shard == "batch" else a.batch) / (ms_sus * 1e-3),
+                     "note": "second half of a back-to-back run of the timed step",
+                     "clocks": sclk.summary()}
     algo = w.bytes_per_launch()
     pk = peaks()
     achieved = algo / (ms_attn_layer * 1e-3) / 1e9
@@ -386,6 +407,7 @@ def run_ours(a, rank: int, world: int, dist) -> dict | None:
             "traffic": ncu_traffic(),
         },
         "clocks": clk.summary(),
+        "sustained": sustained,
         "gpu_launches": a.steps * w.launches_per_step(),
         "global_batch": global_batch,
     }
@@ -562,6 +584,7 @@ def main() -> None:
             "e2e": {"value": res["e2e_value"], "unit": "tokens/s", "ms_per_step": res["e2e_ms"],
                     "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"]},
             "clocks": res["clocks"],
+            "sustained": res.get("sustained"),
             "gpu_launches": res["gpu_launches"],
             "extras": res.get("extras"),
         }

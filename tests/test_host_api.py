@@ -118,3 +118,18 @@ def test_product_never_imports_oracle():
     for f in pkg.rglob("*.py"):
         src = f.read_text()
         assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_value_bits_validation_without_gpu():
+    """The batched cache's value-quantization mode checks its arguments before
+    it touches a device (same ValueError as quantize_uniform's bit check)."""
+    import pytest
+
+    import paper_2502_00527_b200 as pq
+
+    with pytest.raises(ValueError):
+        pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 128, 0, value_bits=9)
+    with pytest.raises(ValueError):
+        pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 128, 0, value_bits=2)
+    with pytest.raises(ValueError):
+        pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 64, 0, value_bits=4)
