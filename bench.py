@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--shard", choices=["batch", "heads"], default="batch")
+    ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
+                    help="head sharding: fused peer-store gather in the decode epilogue, or NCCL all-gather")
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--batch", type=int, default=16)
     ap.add_argument("--ctx", type=int, default=32768)
@@ -213,7 +215,7 @@ class DecodeWorkload:
     layer's fused decode (optionally followed by the head-output gather)."""
 
     def __init__(self, dev, *, layers, batch, hq, hkv, T, m, n, page_tokens, seed, plan=None, group=None,
-                 value_bits=None):
+                 value_bits=None, gather="p2p"):
         import torch
 
         import paper_2502_00527_b200 as pq
@@ -242,12 +244,23 @@ class DecodeWorkload:
         self.out = torch.empty((layers, self.upl, self.G, 128), dtype=torch.bfloat16, device=dev)
         self.views = [self.cache.view(i * self.upl, (i + 1) * self.upl) for i in range(layers)]
         self.gathered = None
-        if plan is not None:
+        self.peers = None
+        if plan is not None and gather == "p2p":  # fused into the decode epilogue (peer stores + flags)
+            from paper_2502_00527_b200.sharding import PeerGather
+
+            self.peers = PeerGather(plan, dev, group)
+        elif plan is not None:
             self.gathered = torch.empty((layers, batch, hq, 128), dtype=torch.bfloat16, device=dev)
         self.stream = torch.cuda.Stream(device=dev)
         self.base_flags = 0  # PQB_DECODE_* bits added to every launch (kernel-variant probes)
 
     def step(self, flags: int = 0):
+        if self.peers is not None:
+            for i in range(self.L):
+                self.views[i].decode_peer(self.q[i], self.peers.descriptor(i), max_tokens=self.T)
+            for i in range(self.L):
+                self.peers.wait(i)
+            return
         for i in range(self.L):
             self.views[i].decode(self.q[i], out=self.out[i], max_tokens=self.T, flags=flags | self.base_flags)
             if self.gathered is not None:
@@ -329,7 +342,7 @@ def run_ours(a, rank: int, world: int, dist) -> dict | None:
         shape = sharding.DecodeShape(a.layers, a.batch, a.hq, a.hkv)
         plan = sharding.head_shard(shape, world, rank)
     w = DecodeWorkload(dev, layers=a.layers, batch=batch, hq=a.hq, hkv=a.hkv, T=a.ctx, m=a.m, n=a.n,
-                       page_tokens=a.page_tokens, seed=rank, plan=plan)
+                       page_tokens=a.page_tokens, seed=rank, plan=plan, gather=a.gather)
     from paper_2502_00527_b200 import _lib as _l
 
     w.base_flags = {"auto": 0, "lut": _l.PQB_DECODE_LUT, "dq": _l.PQB_DECODE_DQ}[a.variant]
@@ -531,7 +544,9 @@ def main() -> None:
               "global_batch": a.batch * world if not heads else a.batch,
               "q_heads": a.hq, "kv_heads": a.hkv, "head_dim": 128, "angle_bits": a.m, "radius_bits": a.n,
               "page_tokens": a.page_tokens,
-              "parallelism": (f"kv-head sharded x{world} + per-layer NCCL all-gather" if heads
+              "parallelism": (f"kv-head sharded x{world} + per-layer head gather "
+                              + ("fused into the decode epilogue (peer stores over NVLink)" if a.gather == "p2p"
+                                 else "(NCCL all-gather)") if heads
                               else f"batch-sharded x{world} (no collective)"),
               "l2": "inputs (43 GB cache per GPU) >> 126 MB L2; no flush needed"}
 

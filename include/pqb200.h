@@ -205,6 +205,34 @@ int pqb_decode_attn_ex(const pqb_cache* cache, int64_t n_units, int group, const
                        float* scores, int64_t scores_ld, void* workspace, size_t workspace_bytes,
                        int flags, int splits, pqb_stream_t stream);
 /* Split count the automatic policy picks (for workspace sizing / reporting). */
+/*
+ * Head-output gather fused into the decode epilogue (KV-head-sharded layers,
+ * SURVEY 8(e); replaces the per-layer NCCL all-gather of [B, Hq, d]): every
+ * output row is stored straight into each peer's gathered buffer
+ * [batch][q_heads][128] through peer pointers (NVLink P2P / CUDA IPC), and the
+ * grid's last CTA then increments flags[rank] in every peer's flag array
+ * (fence + release add, system scope; counting, so CUDA-graph replays work).  Unit u of the call is
+ * (sequence batch0 + u / kv_local, kv head head0 + u % kv_local); query g of it
+ * is head (head0 + u % kv_local) * group + g.  DQ kernel only (group 4 or 8,
+ * d = 128); the workspace is the same as pqb_decode_attn's.
+ */
+#define PQB_MAX_PEERS 8
+typedef struct pqb_peer_out {
+  void* out[PQB_MAX_PEERS];       /* peer k's gathered buffer of this layer (out[rank]: local) */
+  uint32_t* flags[PQB_MAX_PEERS]; /* peer k's flag array [n_peers] of this layer */
+  int32_t n_peers, rank;
+  int32_t batch0, head0, kv_local, q_heads;
+  int32_t out_dtype;              /* PQB_F32 or PQB_BF16 */
+  int32_t reserved;
+} pqb_peer_out;
+int pqb_decode_attn_peer(const pqb_cache* cache, int64_t n_units, int group, const void* q, int q_dtype,
+                         float sm_scale, int max_tokens, const pqb_peer_out* peer, void* workspace,
+                         size_t workspace_bytes, pqb_stream_t stream);
+/* Enqueue on `stream`: ++*expect (device counter of this layer), then wait until
+ * flags[k] >= *expect for every k != rank (acquire loads, system scope).  After
+ * it the layer's gathered buffer is complete. */
+int pqb_peer_wait(const uint32_t* flags, int n_peers, int rank, uint32_t* expect, pqb_stream_t stream);
+
 int pqb_decode_splits(int64_t n_units, int max_tokens);
 
 /* ------------------------------------------------------------ accessors ----

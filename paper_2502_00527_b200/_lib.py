@@ -63,6 +63,26 @@ class PqbCache(ctypes.Structure):
     ]
 
 
+PQB_MAX_PEERS = 8
+
+
+class PqbPeerOut(ctypes.Structure):
+    """pqb_peer_out (include/pqb200.h): the fused head-output gather of a layer."""
+
+    _fields_ = [
+        ("out", c_vp * PQB_MAX_PEERS),
+        ("flags", c_vp * PQB_MAX_PEERS),
+        ("n_peers", c_i32),
+        ("rank", c_i32),
+        ("batch0", c_i32),
+        ("head0", c_i32),
+        ("kv_local", c_i32),
+        ("q_heads", c_i32),
+        ("out_dtype", c_i32),
+        ("reserved", c_i32),
+    ]
+
+
 # name -> (restype, argtypes); must match include/pqb200.h exactly
 SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "pqb_abi_version": (c_i32, []),
@@ -105,6 +125,12 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
          c_vp, c_sz, c_i32, c_i32, c_vp],
     ),
     "pqb_decode_splits": (c_i32, [c_i64, c_i32]),
+    "pqb_decode_attn_peer": (
+        c_i32,
+        [ctypes.POINTER(PqbCache), c_i64, c_i32, c_vp, c_i32, c_f32, c_i32, ctypes.POINTER(PqbPeerOut), c_vp, c_sz,
+         c_vp],
+    ),
+    "pqb_peer_wait": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp]),
     "pqb_angle_table": (c_i32, [c_i32, c_vp, c_vp, c_vp]),
     "pqb_query_lut": (c_i32, [c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "pqb_radius_table": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp]),

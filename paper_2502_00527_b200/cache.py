@@ -448,6 +448,21 @@ class UnitView:
         )
         return out
 
+    def decode_peer(self, q, peer: "_lib.PqbPeerOut", sm_scale: float | None = None,
+                    max_tokens: int | None = None) -> None:
+        """Fused decode + head-output gather (pqb_decode_attn_peer): outputs go
+        straight into every peer's gathered buffer described by ``peer``."""
+        c = self.cache
+        q = self._check_q(q)
+        G = q.shape[1]
+        T_max = int(max_tokens if max_tokens is not None else self.max_tokens)
+        if T_max <= 0:
+            raise ValueError("cannot attend over an empty cache")
+        ws = self.workspace(G, T_max)
+        scale = (1.0 / math.sqrt(c.dim)) if sm_scale is None else float(sm_scale)
+        _lib.call("pqb_decode_attn_peer", self.ref, self.n_units, G, ptr(q), dtype_code(q), scale, T_max,
+                  ctypes.byref(peer), ptr(ws), ws.numel(), stream_ptr(c.device))
+
     def scores(self, q, max_tokens: int | None = None, *, flags: int = 0) -> torch.Tensor:
         c = self.cache
         q = self._check_q(q)

@@ -223,6 +223,38 @@ int pqb_decode_attn(const pqb_cache* cache, int64_t n_units, int group, const vo
                             scores_ld, workspace, workspace_bytes, 0, 0, stream);
 }
 
+int pqb_decode_attn_peer(const pqb_cache* cache, int64_t n_units, int group, const void* q, int q_dtype,
+                         float sm_scale, int max_tokens, const pqb_peer_out* peer, void* workspace,
+                         size_t workspace_bytes, pqb_stream_t stream) {
+  PQB_CHECK(peer != nullptr, PQB_EINVAL, "null peer descriptor");
+  PQB_CHECK(peer->n_peers >= 1 && peer->n_peers <= PQB_MAX_PEERS && peer->rank >= 0 && peer->rank < peer->n_peers,
+            PQB_EINVAL, "bad peer count / rank");
+  PQB_CHECK(peer->kv_local >= 1 && peer->q_heads >= group && peer->batch0 >= 0 && peer->head0 >= 0, PQB_EINVAL,
+            "bad peer layout");
+  PQB_CHECK(peer->out_dtype == PQB_F32 || peer->out_dtype == PQB_BF16, PQB_EINVAL, "bad peer out dtype");
+  for (int k = 0; k < peer->n_peers; ++k)
+    PQB_CHECK(peer->out[k] && peer->flags[k], PQB_EINVAL, "null peer buffer %d", k);
+  PQB_CHECK(cache != nullptr, PQB_EINVAL, "null cache");
+  PQB_CHECK(cache->scales && cache->seq_lens && cache->quant_lens, PQB_ESTATE, "cache is empty; prefill first");
+  PQB_CHECK(q && dtype_ok(q_dtype), PQB_EINVAL, "bad query");
+  PQB_CHECK(max_tokens >= 1 && n_units >= 0 && n_units <= 65535, PQB_EINVAL, "bad token / unit count");
+  const int rc = check_store(&cache->store, cache->d, cache->angle_bits, cache->radius_bits, true);
+  if (rc) return rc;
+  if (n_units == 0) return PQB_OK;
+  DecodeArgs a{cache, n_units, group, q, q_dtype, sm_scale, max_tokens, peer->out[peer->rank], peer->out_dtype,
+               nullptr, 0, workspace, workspace_bytes, 0, 0, peer};
+  const int lrc = launch_decode(a, reinterpret_cast<cudaStream_t>(stream));
+  if (lrc) return lrc;
+  return cuda_status("pqb_decode_attn_peer");
+}
+
+int pqb_peer_wait(const uint32_t* flags, int n_peers, int rank, uint32_t* expect, pqb_stream_t stream) {
+  PQB_CHECK(flags && expect && n_peers >= 1 && n_peers <= PQB_MAX_PEERS && rank >= 0 && rank < n_peers, PQB_EINVAL,
+            "bad peer wait arguments");
+  launch_peer_wait(flags, n_peers, rank, expect, reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status("pqb_peer_wait");
+}
+
 int pqb_decode_splits(int64_t n_units, int max_tokens) {
   if (n_units <= 0 || max_tokens <= 0) return 1;
   return decode_splits(n_units, max_tokens);

@@ -548,7 +548,10 @@ int decode_splits(int64_t n_units, int max_tokens) { return choose_splits(n_unit
 // workspace: [counters: n_units ints, 256-B rounded][partials: n_units * slots * G * (2 + d) floats]
 // The counter region sits at a fixed offset for a given n_units, is zero before
 // the first call and is left zeroed by every fused call.
-static size_t counter_bytes(int64_t n_units) { return (static_cast<size_t>(n_units) * sizeof(int) + 255) / 256 * 256; }
+// one counter per unit (split merge) + the grid-done counter of peer mode
+static size_t counter_bytes(int64_t n_units) {
+  return (static_cast<size_t>(n_units + 1) * sizeof(int) + 255) / 256 * 256;
+}
 
 static size_t partial_bytes(int64_t n_units, int group, int max_tokens, int d) {
   const int s = std::max(max_splits(max_tokens), fast_slots(n_units, max_tokens));
@@ -571,6 +574,9 @@ static int fast_setup(const DecodeArgs& a, EpiArgs& ep, WorkSplit& ws, int& grid
   ep.part_ml = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + counter_bytes(a.n_units));
   ep.part_o = ep.part_ml + a.n_units * ep.slots * a.group * 2;
   ep.merge = !(a.flags & PQB_DECODE_NO_COMBINE);
+  ep.group = a.group;
+  ep.peer_mode = a.peer != nullptr;
+  if (a.peer) ep.peer = *a.peer;
   if (a.out != nullptr) {
     const size_t need = decode_workspace_bytes(a.n_units, a.group, a.max_tokens, 128);
     if (a.workspace == nullptr || a.workspace_bytes < need) {
@@ -660,6 +666,10 @@ int launch_decode(const DecodeArgs& a, cudaStream_t s) {
     const int rc = launch_dq_path(a, s, handled);
     if (rc != PQB_OK) return rc;
   }
+  if (a.peer != nullptr && !handled) {
+    set_error("peer-gather decode needs the DQ kernel (group 4 or 8, d = 128, a fast-path store and bit widths)");
+    return PQB_EUNSUPPORTED;
+  }
   if (fast_ok && !handled && !vq && !(a.flags & PQB_DECODE_FORCE_GENERIC)) {
     // scores requested -> the bit-exact scoring sequence; fused-only -> FMA form
     const int rc = a.scores != nullptr ? dispatch_fast<true>(a, s, handled) : dispatch_fast<false>(a, s, handled);
@@ -675,6 +685,8 @@ int launch_decode(const DecodeArgs& a, cudaStream_t s) {
   EpiArgs ep;
   ep.out = a.out;
   ep.out_dtype = a.out_dtype;
+  ep.group = a.group;
+  ep.peer_mode = false;
   ep.slots = splits;
   // partials after the (untouched) counter region of the fast path
   ep.part_ml = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + counter_bytes(a.n_units));

@@ -149,11 +149,43 @@ struct EpiArgs {
   int* counters;   // [n_units] finished-segment counts (zero between calls)
   int slots;       // partial slots per unit
   bool merge;      // fast kernel: last CTA of a unit merges (else leave partials)
+  bool peer_mode;  // outputs go to every peer's gathered buffer (pqb_decode_attn_peer)
+  int group;       // queries per unit (peer-mode destination index)
+  pqb_peer_out peer;
 };
 
 PQB_DEV void store_out(void* out, int dt, int64_t idx, float v) {
   if (dt == PQB_F32) static_cast<float*>(out)[idx] = v;
   else static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
+}
+
+// Output element (unit, query g, dim e): the local [unit][G][128] array, or in
+// peer mode row (sequence, q head) of every peer's gathered [B][Hq][128] buffer.
+PQB_DEV void emit(const EpiArgs& ep, int64_t unit, int g, int e, float v) {
+  if (!ep.peer_mode) {
+    store_out(ep.out, ep.out_dtype, (unit * ep.group + g) * 128 + e, v);
+    return;
+  }
+  const int64_t b = ep.peer.batch0 + unit / ep.peer.kv_local;
+  const int64_t hq = (ep.peer.head0 + unit % ep.peer.kv_local) * ep.group + g;
+  const int64_t idx = (b * ep.peer.q_heads + hq) * 128 + e;
+  for (int k = 0; k < ep.peer.n_peers; ++k) store_out(ep.peer.out[k], ep.peer.out_dtype, idx, v);
+}
+
+// Peer mode, end of the kernel: once every CTA has stored its outputs (each
+// fences at system scope before counting itself done), the last one increments
+// flags[rank] in every peer's flag array (release, system scope).  grid_done
+// lives in the workspace counter region and is left zeroed.  Caller: all threads.
+PQB_DEV void peer_publish(const EpiArgs& ep, int* grid_done, int tid) {
+  if (!ep.peer_mode) return;
+  __threadfence_system();
+  __syncthreads();
+  if (tid == 0 && atomicAdd(grid_done, 1) == static_cast<int>(gridDim.x) - 1) {
+    __threadfence_system();
+    for (int k = 0; k < ep.peer.n_peers; ++k)
+      asm volatile("red.release.sys.global.add.u32 [%0], 1;" ::"l"(ep.peer.flags[k] + ep.peer.rank) : "memory");
+    *grid_done = 0;
+  }
 }
 
 // Persistent work split: items = n_units * tiles_max, CTA c owns
@@ -203,7 +235,7 @@ PQB_DEV void merge_slots(const EpiArgs& ep, int64_t unit, int nseg, int G, int t
       }
       mx = bm;
     }
-    store_out(ep.out, ep.out_dtype, (unit * G + g) * 128 + e, O / L);
+    emit(ep, unit, g, e, O / L);
   }
 }
 
@@ -237,7 +269,7 @@ PQB_DEV void finish_segment(const EpiArgs& ep, const WorkSplit& ws, int64_t unit
       }
     }
     if (direct && ep.merge) {
-      store_out(ep.out, ep.out_dtype, (unit * G + g) * 128 + e, O / L);
+      emit(ep, unit, g, e, O / L);
     } else {
       ep.part_o[(slot + g) * 128 + e] = O;
       if (e == 0) {

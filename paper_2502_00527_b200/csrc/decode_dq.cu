@@ -578,6 +578,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     }
     finish_segment<G>(ep, ws, unit, red, s_misc + 1, tid, blockDim.x);
   }
+  peer_publish(ep, ep.counters + ws.items / ws.tiles_max, tid);
 }
 
 // ------------------------------------------------------------------ host side

@@ -53,6 +53,7 @@ struct DecodeArgs {
   size_t workspace_bytes;
   int flags = 0;   // PQB_DECODE_* bits
   int splits = 0;  // 0: automatic
+  const pqb_peer_out* peer = nullptr;  // pqb_decode_attn_peer
 };
 
 int launch_radius_scales(const RadiusScalesArgs& a, cudaStream_t s);
@@ -83,6 +84,7 @@ int launch_read_values(const pqb_store& st, int64_t unit, int d, int64_t T, floa
 int launch_pack_codes(const uint8_t* a, const uint8_t* r, int64_t T, int d, int m, int n, const pqb_store& st,
                       int64_t unit, cudaStream_t s);
 int launch_dequantize(const pqb_cache& c, int64_t unit, int64_t T, float* out, cudaStream_t s);
+int launch_peer_wait(const uint32_t* flags, int n_peers, int rank, uint32_t* expect, cudaStream_t s);
 int launch_quantize_values(const void* vals, int dt, int64_t n, int d, int bits, float* out, cudaStream_t s);
 int launch_softmax_f64(const float* scores, int64_t n, double temperature, double* out, cudaStream_t s);
 int launch_synthetic_keys(uint64_t seed, int64_t n_units, int64_t T, int d, int layout, float mu, float sigma,

@@ -331,6 +331,27 @@ int launch_dequantize(const pqb_cache& c, int64_t unit, int64_t T, float* out, c
   return 0;
 }
 
+// pqb_peer_wait: one thread bumps this layer's expected count, then spins
+// (acquire, system scope) until every other rank's count has reached it.
+__global__ void peer_wait_kernel(const uint32_t* flags, int n_peers, int rank, uint32_t* expect) {
+  const uint32_t e = *expect + 1u;
+  *expect = e;
+  for (int k = 0; k < n_peers; ++k) {
+    if (k == rank) continue;
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + k) : "memory");
+      if (static_cast<int32_t>(v - e) >= 0) break;
+      __nanosleep(100);
+    }
+  }
+}
+
+int launch_peer_wait(const uint32_t* flags, int n_peers, int rank, uint32_t* expect, cudaStream_t s) {
+  peer_wait_kernel<<<1, 1, 0, s>>>(flags, n_peers, rank, expect);
+  return 0;
+}
+
 int launch_quantize_values(const void* vals, int dt, int64_t n, int d, int bits, float* out, cudaStream_t s) {
   if (n) quantize_values_kernel<<<static_cast<unsigned>((n + 7) / 8), 256, 0, s>>>(vals, dt, n, d, bits, out);
   return 0;

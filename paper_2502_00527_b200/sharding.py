@@ -12,6 +12,11 @@ hq // G), so the cache shards without any data-path exchange:
                      per-layer [B, Hq, d] output is all-gathered (NCCL over
                      NVLink on the GPU box; gloo in the CPU tests).  This is the
                      only collective on the path (configs[2], configs[3]).
+                     ``gather="p2p"`` fuses it into the decode kernel instead:
+                     the epilogue stores each output row into every rank's
+                     gathered buffer through CUDA IPC peer pointers and the
+                     grid's last CTA publishes a per-(layer, rank) flag
+                     (PeerGather, pqb_decode_attn_peer / pqb_peer_wait).
 """
 
 from __future__ import annotations
@@ -137,21 +142,91 @@ def plan_for(shape: DecodeShape, world: int, rank: int, head: bool) -> ShardPlan
     return head_shard(shape, world, rank) if head else batch_shard(shape, world, rank)
 
 
+class PeerGather:
+    """Gathered per-layer outputs [L, B, Hq, d] shared by the ranks of one node.
+
+    Every rank allocates its own buffer and a flag array [L, world] (uint32,
+    zero), then all ranks exchange CUDA IPC handles (torch's CUDA tensor
+    reduction, sent through ``dist.all_gather_object``) and open each other's
+    buffers, so the decode epilogue can store into all of them directly."""
+
+    def __init__(self, plan: ShardPlan, device, group=None, dtype=torch.bfloat16) -> None:
+        import torch.distributed as dist
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        S = plan.shape
+        if plan.world > 8:
+            raise ValueError("peer gather supports up to 8 ranks")
+        self.plan, self.dtype = plan, dtype
+        self.out = torch.zeros((S.layers, S.batch, S.q_heads, S.head_dim), dtype=dtype, device=device)
+        self.flags = torch.zeros((S.layers, plan.world), dtype=torch.int32, device=device)  # counts, peers add
+        self.expect = torch.zeros(S.layers, dtype=torch.int32, device=device)  # this rank's per-layer count
+        torch.cuda.synchronize(device)
+        mine = (reduce_tensor(self.out), reduce_tensor(self.flags))
+        handles = [None] * plan.world
+        dist.all_gather_object(handles, mine, group=group)
+        self.peer_out, self.peer_flags = [], []
+        for r, (ho, hf) in enumerate(handles):
+            if r == plan.rank:
+                self.peer_out.append(self.out)
+                self.peer_flags.append(self.flags)
+            else:
+                self.peer_out.append(ho[0](*ho[1]))
+                self.peer_flags.append(hf[0](*hf[1]))
+        self._desc = [self._descriptor(layer) for layer in range(S.layers)]
+
+    def descriptor(self, layer: int):
+        return self._desc[layer]
+
+    def _descriptor(self, layer: int):
+        from . import _lib
+        from ._device import dtype_code
+
+        p, S = self.plan, self.plan.shape
+        d = _lib.PqbPeerOut()
+        for k in range(p.world):
+            d.out[k] = self.peer_out[k][layer].data_ptr()
+            d.flags[k] = self.peer_flags[k][layer].data_ptr()
+        d.n_peers, d.rank = p.world, p.rank
+        d.batch0, d.head0, d.kv_local, d.q_heads = p.b0, p.h0, p.kv_heads, S.q_heads
+        d.out_dtype = dtype_code(self.out)
+        return d
+
+    def wait(self, layer: int) -> None:
+        """Enqueue the wait for every rank's layer output (replay-safe: counts)."""
+        from . import _lib
+        from ._device import ptr, stream_ptr
+
+        _lib.call("pqb_peer_wait", ptr(self.flags[layer]), self.plan.world, self.plan.rank, ptr(self.expect[layer:]),
+                  stream_ptr(self.out.device))
+
+
 class HeadShardedDecoder:
-    """Per-rank decode over a head-sharded cache + the per-layer NCCL gather.
+    """Per-rank decode over a head-sharded cache + the per-layer head gather.
 
     ``cache`` is this rank's PolarKVCache holding plan.n_units units in
     plan.unit_index order; ``step(q)`` runs all layers for q [L, B, Hq, d] and
-    returns the gathered [L, B, Hq, d] outputs."""
+    returns the gathered [L, B, Hq, d] outputs.  gather = "nccl" (decode, then
+    the collective) or "p2p" (fused into the decode epilogue, PeerGather)."""
 
-    def __init__(self, cache, plan: ShardPlan, group=None, out_dtype=torch.bfloat16) -> None:
+    def __init__(self, cache, plan: ShardPlan, group=None, out_dtype=torch.bfloat16, gather: str = "nccl") -> None:
+        if gather not in ("nccl", "p2p"):
+            raise ValueError(f"gather must be 'nccl' or 'p2p', got {gather!r}")
         self.cache, self.plan, self.group = cache, plan, group
         upl = plan.units_per_layer
         self.views = [cache.view(layer * upl, (layer + 1) * upl) for layer in range(plan.shape.layers)]
         self.out_dtype = out_dtype
+        self.gather = gather
+        self.peers = PeerGather(plan, cache.device, group, out_dtype) if gather == "p2p" else None
 
-    def layer(self, layer: int, q_layer: torch.Tensor) -> torch.Tensor:
-        local = self.views[layer].decode(local_queries(q_layer, self.plan), out_dtype=self.out_dtype)
+    def layer(self, layer: int, q_layer: torch.Tensor, wait: bool = True) -> torch.Tensor:
+        q_loc = local_queries(q_layer, self.plan)
+        if self.peers is not None:
+            self.views[layer].decode_peer(q_loc, self.peers.descriptor(layer))
+            if wait:
+                self.peers.wait(layer)
+            return self.peers.out[layer]
+        local = self.views[layer].decode(q_loc, out_dtype=self.out_dtype)
         return gather_head_outputs(local, self.plan, self.group)
 
     def step(self, q: torch.Tensor) -> torch.Tensor:
