@@ -70,6 +70,7 @@ def _worker(rank, world, port, G, result_dir):
                 dec.layer(layer, q[layer])
         for _ in range(2):
             dec.peers.out.zero_()
+            torch.cuda.synchronize()
             dist.barrier()  # every rank has cleared its buffer before anyone writes again
             graph.replay()
             torch.cuda.synchronize()
