@@ -422,12 +422,15 @@ def test_dq_page_sizes(page_tokens, G):
     # regression: at G = 8 the end-of-segment merge scratch once overran warp
     # 0's mbarriers (CTAs whose later segments issue TMA: the short third unit)
     lut = cache.decode(qd, flags=pq._lib.PQB_DECODE_LUT).cpu().numpy()
+    scores = cache.scores(qd).cpu().numpy()  # bit-exact qk_scores sequence, every page size
     for u in range(U):
         a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
         s16 = cache.scales16[u].cpu().numpy()
         vb = torch.from_numpy(vals[u]).to(torch.bfloat16).float().numpy().astype(np.float64)
         for g in range(G):
             ref = po.lut_scores(q[u, g], a, r, s16, 4, 4, 1, np.zeros((0, 128), np.float32))
+            ex = exact.lut_scores(q[u, g], a, r, s16, 4, 4, 1)
+            assert np.array_equal(scores[u, g, :lens[u]].view(np.uint32), ex.view(np.uint32))
             o_ref = po.softmax64(ref, 1.0 / math.sqrt(128)) @ vb
             peak_close(out[u, g], o_ref, OUT_RTOL_F32)
             peak_close(lut[u, g], o_ref, OUT_RTOL_F32)
