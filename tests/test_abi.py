@@ -52,6 +52,20 @@ def test_struct_layout_matches_header():
     # pqb_store: 8 + 4*8 + 8 + 4*4 = 64 bytes; pqb_cache: store + 4*4 + 4*8 + 2*4
     assert ctypes.sizeof(_lib.PqbStore) == 64
     assert ctypes.sizeof(_lib.PqbCache) == 64 + 16 + 32 + 8
+    # pqb_peer_out: 8 + 8 pointers, 8 int32
+    assert ctypes.sizeof(_lib.PqbPeerOut) == 16 * 8 + 8 * 4
+
+
+def test_peer_descriptor_validation():
+    """A peer descriptor with a rank outside [0, n_peers) or a missing buffer is
+    rejected before any CUDA work (ValueError)."""
+    d = _lib.PqbPeerOut()
+    d.n_peers, d.rank, d.kv_local, d.q_heads, d.out_dtype = 2, 2, 1, 8, 1
+    rc = _lib.load().pqb_decode_attn_peer(None, 1, 8, None, 1, 1.0, 16, ctypes.byref(d), None, 0, None)
+    assert rc == _lib.PQB_EINVAL
+    d.rank = 0  # now the null buffers are the problem
+    rc = _lib.load().pqb_decode_attn_peer(None, 1, 8, None, 1, 1.0, 16, ctypes.byref(d), None, 0, None)
+    assert rc == _lib.PQB_EINVAL
 
 
 @pytest.mark.parametrize(
@@ -64,6 +78,9 @@ def test_struct_layout_matches_header():
         lambda L: L.pqb_query_lut(None, 0, 1, 8, 1, 4, None, None),
         lambda L: L.pqb_softmax_f64(None, 0, 1.0, None, None),  # empty score vector
         lambda L: L.pqb_angle_table(0, None, None, None),
+        lambda L: L.pqb_peer_wait(None, 2, 0, None, None),  # null flags
+        lambda L: L.pqb_decode_attn_peer(None, 1, 4, None, 1, 1.0, 16, None, None, 0, None),  # null peer
+        lambda L: L.pqb_store_values_ex(None, 1, 1, 1, 7, 0, 0, None, None, 0, None, None),  # odd d
     ],
 )
 def test_validation_maps_to_value_error(call):
