@@ -411,6 +411,7 @@ def run_ours(a, rank: int, world: int, dist) -> dict | None:
             "unit": "GB/s",
             "frac": achieved / pk["hbm_gbs"],
             "peak_source": pk["source"],
+            "frac_vs_8tbs_nameplate": achieved / 8000.0,  # SURVEY 8(d) asks for both denominators
             "kernel": (f"decode_fast_kernel<G={G},M={a.m},N={a.n}> (LUT gather" if a.variant == "lut" or G not in (4, 8)
                        else f"decode_dq_kernel<G={G},M={a.m},N={a.n}> (product-table gather + tensor-core QK")
                       + "; persistent; timed with the in-kernel split merge disabled)",
