@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     }
     float m_run = -INFINITY, l_run = 0.0f;  // query g8 (lanes g8 < G)
     float z_run = 0.0f;                     // VQ: sum_t p_t zp_t of query g8 (lane partial)
+    float b_run = 0.0f;                     // VQ: sum_t of the bf16 hi + lo of p_t scale_t fed to the MMA
     float d[8][4];
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt)
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       const float alpha = fast_exp2(m_run - mn);
       const bool rescale = mn != m_run;
       m_run = mn;
-      float ls = 0.0f, zs = 0.0f;
+      float ls = 0.0f, zs = 0.0f, bs = 0.0f;
       uint32_t phi[4], plo[4];  // bf16x2 (tokens 8 nb + 2 t4, +1)
 #pragma unroll
       for (int nb = 0; nb < 4; ++nb) {
@@ -484,9 +485,16 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
         phi[nb] = *reinterpret_cast<const uint32_t*>(&hi);
         plo[nb] = *reinterpret_cast<const uint32_t*>(&lo);
+        if constexpr (VQ) {
+          const float2 lf = __bfloat1622float2(lo);
+          bs += (hf.x + hf.y) + (lf.x + lf.y);
+        }
       }
       l_run = fmaf(l_run, alpha, ls);
-      if constexpr (VQ) z_run = fmaf(z_run, alpha, zs);
+      if constexpr (VQ) {
+        z_run = fmaf(z_run, alpha, zs);
+        b_run = fmaf(b_run, alpha, bs);
+      }
       if (__any_sync(0xffffffffu, rescale && g8 < G)) {
         const float a0 = __shfl_sync(0xffffffffu, alpha, qc0 * 4), a1 = __shfl_sync(0xffffffffu, alpha, qc1 * 4);
 #pragma unroll
@@ -508,9 +516,11 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       // the P^T B-fragments are the score registers (k-step ks = n-blocks 2ks, 2ks+1)
       if constexpr (VQ) {
         // A fragments straight from the code words: nibble -> bf16 (128 + c) by
-        // OR-ing into the exponent pattern of 128, then - 128 (exact)
+        // OR-ing into the bit pattern of 128.0; the 128 * sum(B) it adds is
+        // removed per query in the epilogue, with sum(B) taken over the exact
+        // bf16 hi + lo values the MMA consumed (b_run), so only fp32
+        // accumulation error (~2^-23 * 128 sum p scale) remains
         const uint32_t* vw = reinterpret_cast<const uint32_t*>(st + Cfg::kABytes + Cfg::kRBytes);
-        const __nv_bfloat162 k128 = __floats2bfloat162_rn(128.0f, 128.0f);
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
 #pragma unroll
@@ -518,11 +528,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
             const uint32_t w = vw[(mt * 2 + ks) * 32 + lane];
             uint32_t a[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const uint32_t b = ((w >> (4 * k)) & 0x000F000Fu) | 0x43004300u;
-              const __nv_bfloat162 v = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&b), k128);
-              a[k] = *reinterpret_cast<const uint32_t*>(&v);
-            }
+            for (int k = 0; k < 4; ++k) a[k] = ((w >> (4 * k)) & 0x000F000Fu) | 0x43004300u;
             mma_bf16(d[mt], a[0], a[1], a[2], a[3], phi[2 * ks], phi[2 * ks + 1]);
             if constexpr (!kPacked) mma_bf16(d[mt], a[0], a[1], a[2], a[3], plo[2 * ks], plo[2 * ks + 1]);
           }
@@ -561,9 +567,12 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) d[mt][k] += __shfl_xor_sync(0xffffffffu, d[mt][k], 2);
     }
-    if constexpr (VQ) {  // + sum_t p_t zp_t of the column's query
+    if constexpr (VQ) {  // + sum_t p_t zp_t - 128 sum_t B_t of the column's query
       z_run += __shfl_xor_sync(0xffffffffu, z_run, 1);
       z_run += __shfl_xor_sync(0xffffffffu, z_run, 2);
+      b_run += __shfl_xor_sync(0xffffffffu, b_run, 1);
+      b_run += __shfl_xor_sync(0xffffffffu, b_run, 2);
+      z_run = fmaf(-128.0f, b_run, z_run);
       const float z0 = __shfl_sync(0xffffffffu, z_run, qc0 * 4), z1 = __shfl_sync(0xffffffffu, z_run, qc1 * 4);
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
