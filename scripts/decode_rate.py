@@ -2,6 +2,7 @@
 decode for three shapes, 8-layer caches, short timed runs; for A/B of library
 builds (PQB_LIB=...) with cool-down between processes."""
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -17,7 +18,7 @@ for name, kw in [("g4", dict(batch=16, hq=32, hkv=8, m=4, n=4)), ("g8", dict(bat
                  ("vq4", dict(batch=16, hq=32, hkv=8, m=4, n=4, value_bits=4)),
                  ("m3n2", dict(batch=8, hq=32, hkv=8, m=3, n=2))]:
     T = 131072 if name == "m3n2" else 32768
-    w = bench.DecodeWorkload(dev, layers=8, T=T, page_tokens=128, seed=0, **kw)
+    w = bench.DecodeWorkload(dev, layers=8, T=T, page_tokens=int(os.environ.get("PQB_PAGE", 128)), seed=0, **kw)
     run = w.capture(lambda: w.step(_lib.PQB_DECODE_NO_COMBINE))
     step = w.capture(w.step)
     a = w.bytes_per_launch()
