@@ -58,7 +58,8 @@ def parse():
     ap.add_argument("--hkv", type=int, default=8)
     ap.add_argument("--m", type=int, default=4)
     ap.add_argument("--n", type=int, default=4)
-    ap.add_argument("--page-tokens", type=int, default=128)
+    ap.add_argument("--page-tokens", type=int, default=256,
+                    help="tokens per cache page (decode per-launch rate vs page: 64 0.95, 128 0.98, 256 1.02, 512 1.03 at G=4; profiles/r01/page_size_sweep.md)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip configs 1/3/4/5 side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
