@@ -175,11 +175,12 @@ PQB_DEV void emit(const EpiArgs& ep, int64_t unit, int g, int e, float v) {
 // Peer mode, end of the kernel: once every CTA has stored its outputs (each
 // fences at system scope before counting itself done), the last one increments
 // flags[rank] in every peer's flag array (release, system scope).  grid_done
-// lives in the workspace counter region and is left zeroed.  Caller: all threads.
-PQB_DEV void peer_publish(const EpiArgs& ep, int* grid_done, int tid) {
+// lives in the workspace counter region and is left zeroed.  Caller: the
+// nthreads threads that stored outputs (named barrier 1).
+PQB_DEV void peer_publish(const EpiArgs& ep, int* grid_done, int tid, int nthreads) {
   if (!ep.peer_mode) return;
   __threadfence_system();
-  __syncthreads();
+  named_sync(1, nthreads);
   if (tid == 0 && atomicAdd(grid_done, 1) == static_cast<int>(gridDim.x) - 1) {
     __threadfence_system();
     for (int k = 0; k < ep.peer.n_peers; ++k)
@@ -243,12 +244,13 @@ PQB_DEV void merge_slots(const EpiArgs& ep, int64_t unit, int nseg, int G, int t
 // max, its row sum and its 128 output accumulators into red[warp][g][132]
 // (m, l, pad, pad, o[128]).  Merge the warps; a CTA covering the whole unit
 // stores the output, otherwise it writes a partial slot and the last CTA to
-// finish the unit LSE-merges the slots.  Caller: all threads, after the
-// red writes (this function starts with a __syncthreads()).
+// finish the unit LSE-merges the slots.  Caller: the nthreads threads
+// (tid < nthreads) that wrote red, after the red writes; it synchronises them
+// on named barrier 1.
 template <int G>
 PQB_DEV void finish_segment(const EpiArgs& ep, const WorkSplit& ws, int64_t unit, const float* red, int* s_flag,
                             int tid, int nthreads) {
-  __syncthreads();
+  named_sync(1, nthreads);
   const int64_t c_first = first_cta(ws, unit);
   const int nseg = static_cast<int>(last_cta(ws, unit) - c_first + 1);
   const bool direct = nseg == 1;
@@ -280,9 +282,9 @@ PQB_DEV void finish_segment(const EpiArgs& ep, const WorkSplit& ws, int64_t unit
   }
   if (direct || !ep.merge) return;
   __threadfence();
-  __syncthreads();
+  named_sync(1, nthreads);
   if (tid == 0) *s_flag = atomicAdd(ep.counters + unit, 1) == nseg - 1;
-  __syncthreads();
+  named_sync(1, nthreads);
   if (*s_flag) {
     __threadfence();
     merge_slots(ep, unit, nseg, G, tid, nthreads);

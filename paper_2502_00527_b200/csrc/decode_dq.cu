@@ -49,6 +49,19 @@
 
 namespace pqb {
 
+// Warp specialisation: a fourth warpgroup of producers (warp kNW + j fills the
+// rings of compute warps j and j + 4, which share its SM sub-partition) takes
+// the TMA issue code off the compute warps; registers are rebalanced with
+// setmaxnreg (compute warps 240, producers 32: 2 x 128 x 240 + 128 x 32 = 64K).
+// PQB_DQ_WS=0 builds the previous layout (lane 0 of each compute warp issues).
+#ifndef PQB_DQ_WS
+#define PQB_DQ_WS 1
+#endif
+constexpr bool kDqWs = PQB_DQ_WS != 0;
+constexpr int kDqThreads = kDqWs ? (kNW + 4) * 32 : kNW * 32;
+constexpr int kConsThreads = kNW * 32;
+static_assert(!kDqWs || kNW == 8, "producer j serves compute warps j and j + 4");
+
 template <int G, int M, int N, int VQ = 0>
 struct DqCfg {
   static constexpr int kABytes = kTile * 8 * M;
@@ -215,7 +228,7 @@ struct TileCursor {
 };
 
 template <int G, int M, int N, int PROBE = 0, int VQ = 0>
-__global__ void __launch_bounds__(kNW * 32, 1)
+__global__ void __launch_bounds__(kDqThreads, 1)
     decode_dq_kernel(const pqb_cache c, const void* __restrict__ q, int q_dtype, float sm_scale_log2, EpiArgs ep,
                      WorkSplit ws) {
   using Cfg = DqCfg<G, M, N, VQ>;
@@ -236,11 +249,15 @@ __global__ void __launch_bounds__(kNW * 32, 1)
   // mbarriers live outside the warp areas: the end-of-segment merge scratch
   // (red, G * 132 floats per warp) aliases the stage memory and, at G = 8,
   // would run over warp 0's barriers if they sat behind its stages
-  __shared__ uint64_t s_bar[kNW][kStages];
-  uint64_t* bar = s_bar[warp];
-  if (lane == 0) {
+  __shared__ uint64_t s_bar[kNW][kStages];    // stage full (TMA transaction count)
+  __shared__ uint64_t s_empty[kNW][kStages];  // stage released by its compute warp (WS)
+  uint64_t* bar = s_bar[warp < kNW ? warp : 0];
+  if (lane == 0 && warp < kNW) {
 #pragma unroll
-    for (int s = 0; s < kStages; ++s) mbar_init(bar + s, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(bar + s, 1);
+      mbar_init(&s_empty[warp][s], 1);
+    }
     fence_mbar_init();
   }
   // product table (once per CTA): PT[(a << N) | r][copy] = (r cos_a, r sin_a) as fp16 hi + lo
@@ -259,6 +276,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
                          h2_bits(__halves2half2(__float2half_rn(static_cast<float>(x - __half2float(xh))),
                                                 __float2half_rn(static_cast<float>(y - __half2float(yh))))));
   }
+  if constexpr (kDqWs) __syncthreads();  // producers helped build the table
   const uint32_t ptab_l = smem_u32(smem) + ((lane & 15) << 3);  // this lane's bank-slot copy
   // Programmatic dependent launch: everything above uses constants only; the
   // cache, q and the outputs may belong to the previous kernel in the stream.
@@ -271,6 +289,51 @@ __global__ void __launch_bounds__(kNW * 32, 1)
   const int64_t i_begin = static_cast<int64_t>(blockIdx.x) * ws.per_cta;
   const int64_t i_end = min(ws.items, i_begin + ws.per_cta);
   uint32_t k_iter = 0;
+
+  if constexpr (kDqWs) {
+    if (warp >= kNW) {  // ---- producer warpgroup
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+      const int w0 = warp - kNW, w1 = w0 + 4;
+      uint32_t it0 = 0, it1 = 0;
+      bool first_seg = true;
+      for (int64_t seg = i_begin; seg < i_end;) {
+        const int64_t unit = seg / ws.tiles_max;
+        const int t_lo = static_cast<int>(seg - unit * ws.tiles_max);
+        const int64_t seg_end = min(i_end, (unit + 1) * ws.tiles_max);
+        seg = seg_end;
+        const int n_tiles = (c.seq_lens[unit] + kTile - 1) / kTile;
+        const int t_hi = min(static_cast<int>(seg_end - unit * ws.tiles_max), n_tiles);
+        // the previous segment's merge scratch aliases the stages
+        if (!first_seg) named_sync(2, kDqThreads);
+        first_seg = false;
+        if (lane == 0) {
+          TileCursor c0, c1;
+          c0.init(t_lo + w0, tpp);
+          c1.init(t_lo + w1, tpp);
+          auto issue = [&](int w, uint32_t it, const TileCursor& cu) {
+            const uint32_t s = it % kStages;
+            mbar_wait(&s_empty[w][s], ((it / kStages) & 1) ^ 1);
+            fence_proxy_async_smem();
+            issue_tile_dq<M, N, VQ>(warp_area + w * Cfg::kWarpBytes + s * Cfg::kStageBytes, c.store,
+                                    page_base_c(c.store, unit, PROBE == 2 ? 0 : cu.pg), PROBE == 2 ? 0 : cu.tin,
+                                    &s_bar[w][s]);
+          };
+          while (c0.tile < t_hi) {  // c1 runs 4 tiles behind c0's stream position, never past it
+            issue(w0, it0++, c0);
+            c0.next(dpg, dtin, tpp);
+            if (c1.tile < t_hi) {
+              issue(w1, it1++, c1);
+              c1.next(dpg, dtin, tpp);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      if (!first_seg) named_sync(2, kDqThreads);
+      return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
+  }
 
   const int g8 = lane >> 2, t4 = lane & 3;  // fragment group / thread-in-group
   const uint32_t ld_row = static_cast<uint32_t>((((lane >> 4) & 1) * 8 + (lane & 7)) * 256);
@@ -287,15 +350,15 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     const int n_tiles = (T + kTile - 1) / kTile;
     const int t_hi = min(static_cast<int>(seg_end - unit * ws.tiles_max), n_tiles);
 
-    __syncthreads();  // previous segment is done with q_s / qfrag / merge area
+    named_sync(1, kConsThreads);  // previous segment is done with q_s / qfrag / merge area
     const int first = t_lo + warp;
     // ---- unit setup: q rows, max |q * s|, then the Q' hi/lo A-fragments
     if (tid == 0) s_misc[0] = 0;
-    for (int i = tid; i < G * 128; i += blockDim.x) q_s[i] = load_q(q, q_dtype, unit * G * 128 + i);
-    __syncthreads();
+    for (int i = tid; i < G * 128; i += kConsThreads) q_s[i] = load_q(q, q_dtype, unit * G * 128 + i);
+    named_sync(1, kConsThreads);
     {
       float mx = 0.0f;
-      for (int i = tid; i < G * 128; i += blockDim.x) {
+      for (int i = tid; i < G * 128; i += kConsThreads) {
         const int e = i & 127;
         const int j = c.layout == PQB_HALF_SPLIT ? (e & 63) : (e >> 1);
         mx = fmaxf(mx, fabsf(q_s[i] * half_bits_to_f32(c.scales[unit * 64 + j])));
@@ -303,14 +366,14 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       mx = warp_max(mx);
       if (lane == 0) atomicMax(s_misc, __float_as_int(mx));  // non-negative floats order as ints
     }
-    __syncthreads();
+    named_sync(1, kConsThreads);
     const float qmax = __int_as_float(s_misc[0]);
     // 2^e * qmax in [2^14, 2^15)
     const int e_sc = (qmax > 0.0f && qmax < INFINITY)
                          ? max(-90, min(90, 14 - (static_cast<int>((__float_as_uint(qmax) >> 23) & 0xff) - 127)))
                          : 0;
     // A-fragment rows: g < 8 -> Q'_hi of query g, 8 + g -> Q'_lo of query g (zero for g >= G)
-    for (int i = tid; i < 16 * 32; i += blockDim.x) {
+    for (int i = tid; i < 16 * 32; i += kConsThreads) {
       const int ks = i >> 5, ln = i & 31, g = ln >> 2, t = ln & 3;
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
       if (g < G) {
@@ -326,7 +389,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       }
       qfrag[i] = v;
     }
-    __syncthreads();
+    named_sync(1, kConsThreads);
     uint32_t aq[16][4];
 #pragma unroll
     for (int ks = 0; ks < 16; ++ks) {
@@ -341,7 +404,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
     // ---- lane 0 fills this warp's ring with its first tiles
     TileCursor cur;
     cur.init(first, tpp);
-    if (lane == 0) {
+    if (!kDqWs && lane == 0) {
 #pragma unroll
       for (int s = 0; s < kStages; ++s) {
         if (cur.tile < t_hi) {
@@ -371,7 +434,9 @@ __global__ void __launch_bounds__(kNW * 32, 1)
       const int tok0 = tile * kTile;
       if constexpr (PROBE == 1) {
         __syncwarp();
-        if (lane == 0) {
+        if (kDqWs) {
+          if (lane == 0) mbar_arrive(&s_empty[warp][s]);
+        } else if (lane == 0) {
           if (nt < t_hi) {
             fence_proxy_async_smem();
             issue_tile_dq<M, N, VQ>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, cur.pg), cur.tin,
@@ -547,7 +612,9 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         }
       }
       __syncwarp();
-      if (lane == 0) {
+      if (kDqWs) {
+        if (lane == 0) mbar_arrive(&s_empty[warp][s]);
+      } else if (lane == 0) {
         if (nt < t_hi) {
           fence_proxy_async_smem();
           issue_tile_dq<M, N, VQ>(my_area + s * Cfg::kStageBytes, c.store,
@@ -582,7 +649,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         d[mt][3] += z1;
       }
     }
-    __syncthreads();
+    named_sync(1, kConsThreads);  // every warp is past its last stage read
     float* red = reinterpret_cast<float*>(warp_area);
     float* mine = red + warp * G * 132;
     if (t4 == 0 && g8 < G) {
@@ -601,9 +668,10 @@ __global__ void __launch_bounds__(kNW * 32, 1)
         }
       }
     }
-    finish_segment<G>(ep, ws, unit, red, s_misc + 1, tid, blockDim.x);
+    finish_segment<G>(ep, ws, unit, red, s_misc + 1, tid, kConsThreads);
+    if constexpr (kDqWs) named_arrive(2, kDqThreads);  // producers may refill the stages
   }
-  peer_publish(ep, ep.counters + ws.items / ws.tiles_max, tid);
+  peer_publish(ep, ep.counters + ws.items / ws.tiles_max, tid, kConsThreads);
 }
 
 // ------------------------------------------------------------------ host side
@@ -622,7 +690,7 @@ static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kNW * 32);
+  cfg.blockDim = dim3(kDqThreads);
   cfg.dynamicSmemBytes = Cfg::kSmem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];

@@ -3,6 +3,8 @@ steps, with nvidia-smi sampling SM clock / power / throttle reasons every 50 ms
 (written to gpurun_out/sustain_clocks.csv) to tell a power/clock cause from a
 memory-system one."""
 import json
+import os
+import statistics
 import subprocess
 import sys
 import time
@@ -17,7 +19,7 @@ from paper_2502_00527_b200 import _lib
 flags = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 vbits = int(sys.argv[2]) if len(sys.argv) > 2 else None  # 4: the 4-bit value mode
 dev = torch.device("cuda", 0)
-w = bench.DecodeWorkload(dev, layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, page_tokens=128, seed=0,
+w = bench.DecodeWorkload(dev, layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, page_tokens=int(os.environ.get("PQB_PAGE", 256)), seed=0,
                          value_bits=vbits)
 algo = w.bytes_per_launch()
 run = w.capture(lambda: w.step(_lib.PQB_DECODE_NO_COMBINE | flags))
@@ -40,5 +42,6 @@ for _ in range(3):
     idle_after.append(round(algo / (ms * 1e-3) / 1e9 / 6546.9, 3))
 smi.terminate()
 step_ms = w.timed(w.capture(w.step), 10, 2)
-print(json.dumps({"flags": flags, "value_bits": vbits, "chunk_rates": rates, "after_2s_idle": idle_after,
+print(json.dumps({"flags": flags, "value_bits": vbits, "lib": os.environ.get("PQB_LIB", ""),
+                  "median_last_half": statistics.median(rates[len(rates) // 2:]), "chunk_rates": rates, "after_2s_idle": idle_after,
                   "tokens_per_s_cool": round(w.batch / (step_ms * 1e-3), 1)}))
