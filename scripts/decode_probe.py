@@ -1,6 +1,8 @@
 """Small driver for ncu: a few configs[1]-shaped decode steps (128 units x 32K
 tokens per layer, m4n4, G=4); argv[1] = value bits (0: bf16 values, 4: the
-4-bit value mode), argv[2] = layers."""
+4-bit value mode), argv[2] = layers, argv[3] = g4 (default) | g8 (configs[3]
+per-GPU launch: 32 units of 8 query heads); page size from PQB_PAGE (256)."""
+import os
 import sys
 from pathlib import Path
 
@@ -11,8 +13,10 @@ import bench
 
 vb = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-w = bench.DecodeWorkload(torch.device("cuda", 0), layers=L, batch=16, hq=32, hkv=8, T=32768, m=4, n=4,
-                         page_tokens=128, seed=0, value_bits=vb or None)
+shape = dict(batch=32, hq=8, hkv=1) if (sys.argv[3] if len(sys.argv) > 3 else "g4") == "g8" else dict(
+    batch=16, hq=32, hkv=8)
+w = bench.DecodeWorkload(torch.device("cuda", 0), layers=L, T=32768, m=4, n=4,
+                         page_tokens=int(os.environ.get("PQB_PAGE", 256)), seed=0, value_bits=vb or None, **shape)
 for _ in range(3):
     w.step()
 torch.cuda.synchronize()
