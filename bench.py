@@ -253,6 +253,9 @@ class DecodeWorkload:
         elif plan is not None:
             self.gathered = torch.empty((layers, batch, hq, 128), dtype=torch.bfloat16, device=dev)
         self.stream = torch.cuda.Stream(device=dev)
+        # the prefill ran on the current stream; every decode runs on self.stream
+        self.stream.wait_stream(torch.cuda.current_stream(dev))
+        torch.cuda.synchronize(dev)
         self.base_flags = 0  # PQB_DECODE_* bits added to every launch (kernel-variant probes)
 
     def step(self, flags: int = 0):

@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
             }
           }
         }
-      } else if (tok < T) {  // residual window: fp32 dot (lut_decode.py:107-116)
+      } else if (tok < T && c.res_cap > 0) {  // residual window: fp32 dot (lut_decode.py:107-116)
         const float* kr = c.residual + (unit * c.res_cap + tok % c.res_cap) * 128;
         for (int e = 0; e < 128; ++e) {
           const float kv = kr[e];
@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(256)
           acc[g] = __fadd_rn(acc[g], __fmul_rn(pv, rh));
         }
       }
-    } else if (tok < T) {
+    } else if (tok < T && c.res_cap > 0) {
       const float* kr = c.residual + (unit * c.res_cap + tok % c.res_cap) * d;
       for (int e = 0; e < d; ++e) {
         const float kv = kr[e];

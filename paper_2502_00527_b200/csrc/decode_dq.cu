@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   // would run over warp 0's barriers if they sat behind its stages
   __shared__ uint64_t s_bar[kNW][kStages];    // stage full (TMA transaction count)
   __shared__ uint64_t s_empty[kNW][kStages];  // stage released by its compute warp (WS)
+  __shared__ float s_scale[64];               // the current unit's radius scales
   uint64_t* bar = s_bar[warp < kNW ? warp : 0];
   if (lane == 0 && warp < kNW) {
 #pragma unroll
@@ -261,20 +262,25 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     fence_mbar_init();
   }
   // product table (once per CTA): PT[(a << N) | r][copy] = (r cos_a, r sin_a) as fp16 hi + lo
+  if (tid == 0) s_misc[0] = 0;
   if (tid < (1 << M)) {
     float cf, sf;
     angle_unit(M, tid, cf, sf);
     cs_s[tid] = make_float2(cf, sf);
   }
   __syncthreads();
-  for (int i = tid; i < (16 << (M + N)); i += blockDim.x) {
-    const int e = i >> 4, a = e >> N, r = e & ((1 << N) - 1);
+  // one entry per thread, its 16 bank-slot copies as 8 x 16-byte stores
+  for (int e = tid; e < (1 << (M + N)); e += blockDim.x) {
+    const int a = e >> N, r = e & ((1 << N) - 1);
     const float2 cs = cs_s[a];
     const double x = static_cast<double>(r) * cs.x, y = static_cast<double>(r) * cs.y;  // exact products
     const __half xh = __float2half_rn(static_cast<float>(x)), yh = __float2half_rn(static_cast<float>(y));
-    ptab[i] = make_uint2(h2_bits(__halves2half2(xh, yh)),
-                         h2_bits(__halves2half2(__float2half_rn(static_cast<float>(x - __half2float(xh))),
-                                                __float2half_rn(static_cast<float>(y - __half2float(yh))))));
+    const uint32_t hi = h2_bits(__halves2half2(xh, yh));
+    const uint32_t lo = h2_bits(__halves2half2(__float2half_rn(static_cast<float>(x - __half2float(xh))),
+                                               __float2half_rn(static_cast<float>(y - __half2float(yh)))));
+    uint4* dst = reinterpret_cast<uint4*>(ptab + e * 16);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) dst[k] = make_uint4(hi, lo, hi, lo);
   }
   if constexpr (kDqWs) __syncthreads();  // producers helped build the table
   const uint32_t ptab_l = smem_u32(smem) + ((lane & 15) << 3);  // this lane's bank-slot copy
@@ -353,15 +359,27 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     named_sync(1, kConsThreads);  // previous segment is done with q_s / qfrag / merge area
     const int first = t_lo + warp;
     // ---- unit setup: q rows, max |q * s|, then the Q' hi/lo A-fragments
-    if (tid == 0) s_misc[0] = 0;
-    for (int i = tid; i < G * 128; i += kConsThreads) q_s[i] = load_q(q, q_dtype, unit * G * 128 + i);
+    // one round of independent global loads: the G query rows and the 64 scales
+    // (s_misc[0] is zero here: prologue / reset after the previous fragments)
+    {
+      constexpr int kQPer = G * 128 / kConsThreads;
+      static_assert(kQPer * kConsThreads == G * 128, "q rows per thread");
+      float qv[kQPer];
+#pragma unroll
+      for (int k = 0; k < kQPer; ++k) qv[k] = load_q(q, q_dtype, unit * G * 128 + tid + k * kConsThreads);
+      const float sc = tid < 64 ? half_bits_to_f32(c.scales[unit * 64 + tid]) : 0.0f;
+#pragma unroll
+      for (int k = 0; k < kQPer; ++k) q_s[tid + k * kConsThreads] = qv[k];
+      if (tid < 64) s_scale[tid] = sc;
+    }
     named_sync(1, kConsThreads);
     {
       float mx = 0.0f;
-      for (int i = tid; i < G * 128; i += kConsThreads) {
-        const int e = i & 127;
+#pragma unroll
+      for (int k = 0; k < G * 128 / kConsThreads; ++k) {
+        const int i = tid + k * kConsThreads, e = i & 127;
         const int j = c.layout == PQB_HALF_SPLIT ? (e & 63) : (e >> 1);
-        mx = fmaxf(mx, fabsf(q_s[i] * half_bits_to_f32(c.scales[unit * 64 + j])));
+        mx = fmaxf(mx, fabsf(q_s[i] * s_scale[j]));
       }
       mx = warp_max(mx);
       if (lane == 0) atomicMax(s_misc, __float_as_int(mx));  // non-negative floats order as ints
@@ -378,7 +396,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
       if (g < G) {
         const int j = 16 * t + dq_pair<kFused>(ks);
-        const float sj = half_bits_to_f32(c.scales[unit * 64 + j]);
+        const float sj = s_scale[j];
         const int ex = c.layout == PQB_HALF_SPLIT ? j : 2 * j;
         const int ey = c.layout == PQB_HALF_SPLIT ? j + 64 : 2 * j + 1;
         const float vx = ldexpf(q_s[g * 128 + ex] * sj, e_sc), vy = ldexpf(q_s[g * 128 + ey] * sj, e_sc);
@@ -390,6 +408,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       qfrag[i] = v;
     }
     named_sync(1, kConsThreads);
+    if (tid == 0) s_misc[0] = 0;  // all have read qmax; the next atomicMax is >= 2 barriers later
     uint32_t aq[16][4];
 #pragma unroll
     for (int ks = 0; ks < 16; ++ks) {
@@ -497,7 +516,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         float acc[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) acc[g] = 0.0f;
-        if (tok >= Tq && tok < T) {
+        if (tok >= Tq && tok < T && c.res_cap > 0) {  // (res_cap = 0 implies Tq = T)
           const float* kr = c.residual + (unit * c.res_cap + tok % c.res_cap) * 128;
           for (int e = 0; e < 128; ++e) {
             const float kv = kr[e];

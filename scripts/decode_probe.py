@@ -15,7 +15,7 @@ vb = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 shape = dict(batch=32, hq=8, hkv=1) if (sys.argv[3] if len(sys.argv) > 3 else "g4") == "g8" else dict(
     batch=16, hq=32, hkv=8)
-w = bench.DecodeWorkload(torch.device("cuda", 0), layers=L, T=32768, m=4, n=4,
+w = bench.DecodeWorkload(torch.device("cuda", 0), layers=L, T=int(os.environ.get("PQB_T", 32768)), m=4, n=4,
                          page_tokens=int(os.environ.get("PQB_PAGE", 256)), seed=0, value_bits=vb or None, **shape)
 for _ in range(3):
     w.step()
