@@ -462,6 +462,10 @@ def run_extras(dev, a) -> dict:
         except Exception as exc:  # report, never hide the headline
             out[name] = {"error": f"{type(exc).__name__}: {exc}"}
     try:
+        out["configs[1]_scores_only"] = scores_bench(dev, a)
+    except Exception as exc:
+        out["configs[1]_scores_only"] = {"error": f"{type(exc).__name__}: {exc}"}
+    try:
         out["configs[4]_encode"] = encode_bench(dev, a)
     except Exception as exc:
         out["configs[4]_encode"] = {"error": f"{type(exc).__name__}: {exc}"}
@@ -476,6 +480,41 @@ def ncu_traffic():
         except Exception:
             return None
     return None
+
+
+def scores_bench(dev, a) -> dict:
+    """SURVEY 8(d) scores-only mode (paper Table 4 analogue): configs[1] shape,
+    the bit-exact LUT scores of qk_scores for every query head, all 32 layers.
+    Roofline numerator: the codes (the SURVEY's figure, 8,589,934,592 B/step)
+    and, separately, codes + the fp32 score rows written."""
+    import torch
+
+    w = DecodeWorkload(dev, layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, page_tokens=a.page_tokens,
+                       seed=7)
+    from paper_2502_00527_b200 import _lib
+
+    sc = torch.empty((w.upl, w.G, w.T), dtype=torch.float32, device=dev)
+    codes = w.L * w.upl * (w.T * 64 * (w.m + w.n) // 8)
+    written = w.L * w.upl * w.G * w.T * 4
+    pk = peaks()
+    res = {"codes_bytes_per_step": codes, "scores_bytes_per_step": written, "gpu_launches_per_step": w.L}
+    for name, flags, kern in [
+            ("exact_lut", 0, "decode_fast_kernel EXACT (LUT gather, fp32 channel-order sum, bit-identical to qk_scores)"),
+            ("dq", _lib.PQB_DECODE_DQ, "decode_dq_kernel scores mode (tensor-core QK, within 1e-4 of qk_scores)")]:
+        def step(flags=flags):
+            for i in range(w.L):
+                w.views[i].scores(w.q[i], max_tokens=w.T, out=sc, flags=flags)
+
+        g = w.capture(step)
+        ms = w.timed(g, max(3, a.steps // 2), 2)
+        res[name] = {"kernel": kern, "ms_per_step": ms, "tokens_per_s": w.batch / (ms * 1e-3),
+                     "frac_codes_only": codes / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+                     "frac_codes_plus_scores": (codes + written) / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    del sc
+    w.free()
+    del w
+    torch.cuda.empty_cache()
+    return res
 
 
 def encode_bench(dev, a) -> dict:

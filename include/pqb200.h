@@ -196,7 +196,10 @@ int pqb_decode_attn(const pqb_cache* cache, int64_t n_units, int group, const vo
  * split over tokens (clamped to what the workspace sizing allows). */
 #define PQB_DECODE_FORCE_GENERIC 1 /* use the runtime-shape kernel (testing)          */
 #define PQB_DECODE_NO_COMBINE 2    /* leave split partials in the workspace (timing) */
-#define PQB_DECODE_DQ 4            /* fused call: product-table + tensor-core scoring (default, G 4/8) */
+#define PQB_DECODE_DQ 4            /* fused call: product-table + tensor-core scoring (default, G 4/8);
+                                      scores-only call (out NULL), G 4/8: the same contraction writes
+                                      the score rows, within 1e-4 max(1, peak) of qk_scores instead of
+                                      bit-identical (no softmax, no value bytes)                       */
 #define PQB_DECODE_LUT 8           /* fused call: LUT-gather scoring (default for scores / G = 1)     */
 #define PQB_DECODE_PROBE_MEM 64    /* diagnostics, m4n4 DQ only: stream tiles, skip all compute      */
 #define PQB_DECODE_PROBE_COMPUTE 128 /* diagnostics, m4n4 DQ only: compute on L2-resident tiles      */

@@ -463,12 +463,20 @@ class UnitView:
         _lib.call("pqb_decode_attn_peer", self.ref, self.n_units, G, ptr(q), dtype_code(q), scale, T_max,
                   ctypes.byref(peer), ptr(ws), ws.numel(), stream_ptr(c.device))
 
-    def scores(self, q, max_tokens: int | None = None, *, flags: int = 0) -> torch.Tensor:
+    def scores(self, q, max_tokens: int | None = None, *, flags: int = 0,
+               out: torch.Tensor | None = None) -> torch.Tensor:
         c = self.cache
         q = self._check_q(q)
         G = q.shape[1]
         T_max = int(max_tokens if max_tokens is not None else self.max_tokens)
-        sc = torch.empty((self.n_units, G, max(T_max, 1)), dtype=torch.float32, device=c.device)
+        if out is not None:
+            if (out.dtype != torch.float32 or out.dim() != 3 or tuple(out.shape[:2]) != (self.n_units, G)
+                    or out.shape[2] < T_max or out.stride(2) != 1 or out.stride(1) != out.shape[2]
+                    or out.stride(0) != G * out.shape[2]):
+                raise ValueError(f"out must be a contiguous float32 [{self.n_units}, {G}, >= {T_max}] tensor")
+            sc = out
+        else:
+            sc = torch.empty((self.n_units, G, max(T_max, 1)), dtype=torch.float32, device=c.device)
         if T_max > 0:
             _lib.call(
                 "pqb_decode_attn_ex", self.ref, self.n_units, G, ptr(q), dtype_code(q), 1.0, T_max, None, 0,

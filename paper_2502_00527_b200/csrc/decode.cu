@@ -623,9 +623,12 @@ static int launch_fast(const DecodeArgs& a, cudaStream_t s) {
 // configs[1] launch: 0.87 vs 0.80 of HBM peak at G = 4, 0.66 vs 0.45 at G = 8;
 // the LUT gather is shared-memory bound).  Scores requested, G = 1 or
 // PQB_DECODE_LUT: the LUT kernel (bit-exact qk_scores sequence).
+// Scores-only calls with PQB_DECODE_DQ (G in {4, 8}) take the DQ kernel's
+// scores mode: qk_scores within the stated tolerance instead of bit-identical.
 static bool use_dq(const DecodeArgs& a) {
-  if (a.scores != nullptr || a.out == nullptr || (a.group != 4 && a.group != 8)) return false;
-  if (a.flags & PQB_DECODE_LUT) return false;
+  if (a.group != 4 && a.group != 8) return false;
+  if (a.scores != nullptr) return a.out == nullptr && (a.flags & PQB_DECODE_DQ) && !(a.flags & PQB_DECODE_LUT);
+  if (a.out == nullptr || (a.flags & PQB_DECODE_LUT)) return false;
   return true;
 }
 

@@ -180,19 +180,28 @@ PQB_DEV uint2 lds_u2(uint32_t addr) {
   return v;
 }
 
-// PROBE (diagnostics only, flags PQB_DECODE_PROBE_*): 0 = the kernel; 1 = memory
-// only (tiles stream through the ring, no compute); 2 = compute only (every tile
-// is re-read from the unit's first page, i.e. from L2).
+// PROBE: 0 = the kernel; kDqScores = scores-only mode (qk_scores within the
+// stated tolerance, lut_decode.py:119-154: the QK contraction of the fused
+// kernel, the raw fp32 score rows stored, no softmax / values; only the code
+// bytes are streamed).  Diagnostics (flags PQB_DECODE_PROBE_*): 1 = memory only
+// (tiles stream through the ring, no compute); 2 = compute only (every tile is
+// re-read from the unit's first page, i.e. from L2).
 // VQ: PQB_VQ4 value pages (kv_cache.py:199-209 quantize_values): the P.V MMA
 // takes the 4-bit codes as exact bf16 integers (A) against P * scale (B, hi/lo),
 // and the zero points join as sum_t p_t zp_t per query:
 //   o = sum_t p_t (c_t s_t + z_t) = [codes] . (p s) + sum_t p_t z_t.
-template <int M, int N, int VQ>
+constexpr int kDqScores = 3;
+
+template <int M, int N, int VQ, bool CODES_ONLY = false>
 PQB_DEV void issue_tile_dq(uint8_t* st, const pqb_store& s, const uint8_t* pb, int tin, uint64_t* bar) {
   // tin: tile index within the page (tokens tin * 32 ...)
   constexpr uint32_t kA = kTile * 8 * M, kR = kTile * 8 * N;
   const int in_page = tin * kTile;
-  if constexpr (!VQ) {
+  if constexpr (CODES_ONLY) {
+    mbar_arrive_expect_tx(bar, kA + kR);
+    bulk_g2s(st, pb + s.angle_off + in_page * 8 * M, kA, bar);
+    bulk_g2s(st + kA, pb + s.radius_off + in_page * 8 * N, kR, bar);
+  } else if constexpr (!VQ) {
     constexpr uint32_t kV = kTile * 256;
     mbar_arrive_expect_tx(bar, kA + kR + kV);
     bulk_g2s(st, pb + s.angle_off + in_page * 8 * M, kA, bar);
@@ -230,8 +239,9 @@ struct TileCursor {
 template <int G, int M, int N, int PROBE = 0, int VQ = 0>
 __global__ void __launch_bounds__(kDqThreads, 1)
     decode_dq_kernel(const pqb_cache c, const void* __restrict__ q, int q_dtype, float sm_scale_log2, EpiArgs ep,
-                     WorkSplit ws) {
+                     WorkSplit ws, float* __restrict__ scores, int64_t scores_ld) {
   using Cfg = DqCfg<G, M, N, VQ>;
+  constexpr bool kScores = PROBE == kDqScores;
   constexpr bool kFused = M == 4 && N == 4;
   constexpr bool kPacked = Cfg::kPacked;
   static_assert(G == 1 || G == 2 || G == 4 || G == 8, "G");
@@ -320,7 +330,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             const uint32_t s = it % kStages;
             mbar_wait(&s_empty[w][s], ((it / kStages) & 1) ^ 1);
             fence_proxy_async_smem();
-            issue_tile_dq<M, N, VQ>(warp_area + w * Cfg::kWarpBytes + s * Cfg::kStageBytes, c.store,
+            issue_tile_dq<M, N, VQ, kScores>(warp_area + w * Cfg::kWarpBytes + s * Cfg::kStageBytes, c.store,
                                     page_base_c(c.store, unit, PROBE == 2 ? 0 : cu.pg), PROBE == 2 ? 0 : cu.tin,
                                     &s_bar[w][s]);
           };
@@ -429,7 +439,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         if (cur.tile < t_hi) {
           fence_proxy_async_smem();
           const uint32_t sl = (k_iter + s) % kStages;
-          issue_tile_dq<M, N, VQ>(my_area + sl * Cfg::kStageBytes, c.store,
+          issue_tile_dq<M, N, VQ, kScores>(my_area + sl * Cfg::kStageBytes, c.store,
                                   page_base_c(c.store, unit, PROBE == 2 ? 0 : cur.pg), PROBE == 2 ? 0 : cur.tin,
                                   bar + sl);
         }
@@ -458,7 +468,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         } else if (lane == 0) {
           if (nt < t_hi) {
             fence_proxy_async_smem();
-            issue_tile_dq<M, N, VQ>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, cur.pg), cur.tin,
+            issue_tile_dq<M, N, VQ, kScores>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, cur.pg), cur.tin,
                                     bar + s);
           }
           cur.next(dpg, dtin, tpp);
@@ -535,6 +545,35 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             if (tok0 + r >= Tq) x[nb][j] += rbuf[r * 8 + g8];
           }
         __syncwarp();
+      }
+      if constexpr (kScores) {  // raw scores: x = S * 2^e_sc (exact rescale), tokens 8 nb + 2 t4 + j
+        if (g8 < G) {
+          const float inv_sc = ldexpf(1.0f, -e_sc);
+          float* row = scores + (unit * G + g8) * scores_ld;
+#pragma unroll
+          for (int nb = 0; nb < 4; ++nb) {
+            const int tok = tok0 + 8 * nb + 2 * t4;
+            const float v0 = x[nb][0] * inv_sc, v1 = x[nb][1] * inv_sc;
+            if (tok + 1 < T && (scores_ld & 1) == 0) {
+              __stcs(reinterpret_cast<float2*>(row + tok), make_float2(v0, v1));
+            } else {
+              if (tok < T) row[tok] = v0;
+              if (tok + 1 < T) row[tok + 1] = v1;
+            }
+          }
+        }
+        __syncwarp();
+        if (kDqWs) {
+          if (lane == 0) mbar_arrive(&s_empty[warp][s]);
+        } else if (lane == 0) {
+          if (nt < t_hi) {
+            fence_proxy_async_smem();
+            issue_tile_dq<M, N, VQ, kScores>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, cur.pg),
+                                             cur.tin, bar + s);
+          }
+          cur.next(dpg, dtin, tpp);
+        }
+        continue;
       }
       // ---- online softmax (query g8; the four t4 lanes share it)
       float mx = -INFINITY;
@@ -636,7 +675,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       } else if (lane == 0) {
         if (nt < t_hi) {
           fence_proxy_async_smem();
-          issue_tile_dq<M, N, VQ>(my_area + s * Cfg::kStageBytes, c.store,
+          issue_tile_dq<M, N, VQ, kScores>(my_area + s * Cfg::kStageBytes, c.store,
                                   page_base_c(c.store, unit, PROBE == 2 ? 0 : cur.pg), PROBE == 2 ? 0 : cur.tin,
                                   bar + s);
         }
@@ -644,6 +683,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       }
     }
 
+    if constexpr (kScores) {  // scores-only: nothing to merge
+      if constexpr (kDqWs) named_arrive(2, kDqThreads);
+      continue;
+    }
     // ---- segment epilogue: per-warp (m, l, o) -> shared, then the common merge
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
@@ -718,7 +761,7 @@ static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (cudaLaunchKernelEx(&cfg, decode_dq_kernel<G, M, N, PROBE, VQ>, *a.cache, a.q, a.q_dtype,
-                         a.sm_scale * kLog2e, ep, ws) != cudaSuccess) {
+                         a.sm_scale * kLog2e, ep, ws, a.scores, a.scores_ld) != cudaSuccess) {
     set_error("decode_dq launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     return PQB_ECUDA;
   }
@@ -730,6 +773,17 @@ static int dispatch_dq_mn(const DecodeArgs& a, const EpiArgs& ep, const WorkSpli
                           bool& handled) {
   handled = true;
   const int mn = a.cache->angle_bits * 10 + a.cache->radius_bits;
+  if (a.out == nullptr) {  // scores-only (the caller checked a.scores)
+    switch (mn) {
+      case 44: return launch_dq<G, 4, 4, kDqScores>(a, ep, ws, grid, s);
+      case 32: return launch_dq<G, 3, 2, kDqScores>(a, ep, ws, grid, s);
+      case 22: return launch_dq<G, 2, 2, kDqScores>(a, ep, ws, grid, s);
+      case 42: return launch_dq<G, 4, 2, kDqScores>(a, ep, ws, grid, s);
+      case 24: return launch_dq<G, 2, 4, kDqScores>(a, ep, ws, grid, s);
+      case 34: return launch_dq<G, 3, 4, kDqScores>(a, ep, ws, grid, s);
+      default: handled = false; return PQB_OK;
+    }
+  }
   if (a.cache->store.value_dtype == PQB_VQ4) {
     switch (mn) {
       case 44: return launch_dq<G, 4, 4, 0, 1>(a, ep, ws, grid, s);

@@ -129,6 +129,29 @@ def test_batched_decode_vs_oracle(m, n, G):
             peak_close(out[u, g], w @ v64[u], OUT_RTOL_F32)
 
 
+def test_scores_into_caller_buffer():
+    """UnitView.scores(out=...) (the bench's scores-only mode) writes the same
+    bit-exact rows as the allocating call; bad buffers are rejected."""
+    U, T, G = 3, 1000, 4
+    keys = np.stack([po.synthetic_keys(T, 128, seed=500 + u) for u in range(U)])
+    q = torch.from_numpy(np.random.default_rng(5).standard_normal((U, G, 128)).astype(np.float32)).cuda()
+    cache = pq.PolarKVCache(pq.QuantConfig(4, 4), U, 128, 0, capacity=T)
+    cache.prefill(torch.from_numpy(keys).cuda())
+    ref = cache.scores(q)
+    view = cache.view(0, U)
+    buf = torch.full((U, G, T + 24), 7.0, dtype=torch.float32, device="cuda")  # wider rows: ld = T + 24
+    got = view.scores(q, max_tokens=T, out=buf)
+    assert got.data_ptr() == buf.data_ptr()
+    assert torch.equal(got, ref)
+    assert bool((buf[:, :, T:] == 7.0).all())  # nothing written past max_tokens
+    with pytest.raises(ValueError):
+        view.scores(q, max_tokens=T, out=buf.to(torch.float16))
+    with pytest.raises(ValueError):
+        view.scores(q, max_tokens=T, out=torch.empty((G, U, T), device="cuda").transpose(0, 1))
+    with pytest.raises(ValueError):
+        view.scores(q, max_tokens=T, out=buf[:, :, : T - 1])
+
+
 @pytest.mark.parametrize("T,res", [(32768, 0), (9000, 64), (33, 32), (1, 1), (65, 0)])
 def test_split_and_residual(T, res):
     """Long contexts (many splits), residual windows, tiny / ragged lengths."""
@@ -434,3 +457,27 @@ def test_dq_page_sizes(page_tokens, G):
             o_ref = po.softmax64(ref, 1.0 / math.sqrt(128)) @ vb
             peak_close(out[u, g], o_ref, OUT_RTOL_F32)
             peak_close(lut[u, g], o_ref, OUT_RTOL_F32)
+
+
+@pytest.mark.parametrize("m,n", [(4, 4), (3, 2), (2, 4), (4, 2)])
+@pytest.mark.parametrize("G", [4, 8])
+@pytest.mark.parametrize("T,res,page", [(4096, 0, 256), (1000, 64, 64), (33, 32, 32), (70, 0, 128)])
+def test_dq_scores_mode(m, n, G, T, res, page):
+    """Scores-only calls with PQB_DECODE_DQ (the tensor-core contraction, SURVEY
+    8(c) tolerance) against the bit-exact LUT rows: max|d| <= 1e-4 max(1, peak)
+    per (unit, query) row, residual windows and ragged tails included."""
+    U = 3
+    keys = np.stack([po.synthetic_keys(T, 128, seed=700 + u, outliers=(0, 1)) for u in range(U)])
+    rng = np.random.default_rng(T + G)
+    q = torch.from_numpy(rng.standard_normal((U, G, 128)).astype(np.float32)).to(torch.bfloat16).cuda()
+    cache = pq.PolarKVCache(pq.QuantConfig(m, n), U, 128, res, capacity=T, page_tokens=page, shuffle_pages=True)
+    cache.prefill(torch.from_numpy(keys).cuda())
+    view = cache.view(0, U)
+    exact_rows = view.scores(q).cpu().numpy()
+    fast = view.scores(q, flags=pq._lib.PQB_DECODE_DQ).cpu().numpy()
+    assert fast.shape == exact_rows.shape == (U, G, T)
+    for u in range(U):
+        for g in range(G):
+            tol = 1e-4 * max(1.0, float(np.abs(exact_rows[u, g]).max()))
+            err = float(np.abs(fast[u, g] - exact_rows[u, g]).max())
+            assert err <= tol, (u, g, err, tol)
