@@ -157,6 +157,14 @@ PQB_DEV F2 ffma2(F2 a, F2 b, F2 c) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
   return d;
 }
+PQB_DEV F2 fadd2(F2 a, F2 b) {
+  F2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
 PQB_DEV F2 fmul2(F2 a, F2 b) {
   F2 d;
   asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
@@ -164,6 +172,47 @@ PQB_DEV F2 fmul2(F2 a, F2 b) {
       : "=f"(d.x), "=f"(d.y)
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
+}
+
+// ef_angle of two pairs with the fp32 arithmetic packed (FADD2 / FFMA2 take the
+// |.| and -|.| operand modifiers and broadcast immediates, so |x| +- |y|, the
+// edge tests and the band term cost one instruction per two pairs); every
+// lane value is the IEEE result of the scalar form, so codes and flags are
+// those of ef_angle (which ef_pair_flag re-evaluates).
+template <int M>
+PQB_DEV void ef_angle2(float x0, float x1, float y0, float y1, float& worst, const uint8_t* tab, uint32_t& c0,
+                       uint32_t& c1) {
+  const F2 ax{fabsf(x0), fabsf(x1)}, ay{fabsf(y0), fabsf(y1)};
+  const F2 s = fadd2(ax, ay);
+  const F2 dif = fadd2(ax, F2{-ay.x, -ay.y});
+  const F2 a{fabsf(dif.x), fabsf(dif.y)};
+  uint32_t i0 = __funnelshift_l(__float_as_uint(x0), 0u, 1), i1 = __funnelshift_l(__float_as_uint(x1), 0u, 1);
+  i0 = __funnelshift_l(__float_as_uint(y0), i0, 1);
+  i1 = __funnelshift_l(__float_as_uint(y1), i1, 1);
+  i0 = __funnelshift_l(__float_as_uint(dif.x), i0, 1);
+  i1 = __funnelshift_l(__float_as_uint(dif.y), i1, 1);
+  if constexpr (M == 2) {
+    const F2 t = fadd2(a, F2{-0x1p-100f, -0x1p-100f});
+    i0 = __funnelshift_l(__float_as_uint(t.x), i0, 1);
+    i1 = __funnelshift_l(__float_as_uint(t.y), i1, 1);
+    const F2 b = ffma2(F2{kQuadEdgeThr * 1.01f, kQuadEdgeThr * 1.01f}, s, F2{-a.x, -a.y});
+    worst = fmaxf(worst, fmaxf(fminf(b.x, t.x), fminf(b.y, t.y)));
+  } else {
+    constexpr int NB = 1 << (M - 3);
+    F2 mn{INFINITY, INFINITY};
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const F2 e = ffma2(F2{-a.x, -a.y}, F2{ef_k(M, i), ef_k(M, i)}, s);
+      i0 = __funnelshift_l(__float_as_uint(e.x), i0, 1);
+      i1 = __funnelshift_l(__float_as_uint(e.y), i1, 1);
+      mn.x = fminf(mn.x, fabsf(e.x));
+      mn.y = fminf(mn.y, fabsf(e.y));
+    }
+    const F2 w = ffma2(F2{ef_band_max<M>(), ef_band_max<M>()}, s, F2{-mn.x, -mn.y});
+    worst = fmaxf(worst, fmaxf(w.x, w.y));
+  }
+  c0 = tab[i0];
+  c1 = tab[i1];
 }
 
 // rint(r / s) of two pairs (fast estimate, polar_math.cuh radius_raw_fast).
@@ -430,8 +479,7 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
 #pragma unroll
         for (int i = 0; i < 8; i += 2) {
           ef_radius2(F2{x[i], x[i + 1]}, F2{y[i], y[i + 1]}, F2{inv[i], inv[i + 1]}, rq[i], rq[i + 1], worst_r, rok);
-          ac[i] = ef_angle<M>(x[i], y[i], worst, octant_tab);
-          ac[i + 1] = ef_angle<M>(x[i + 1], y[i + 1], worst, octant_tab);
+          ef_angle2<M>(x[i], x[i + 1], y[i], y[i + 1], worst, octant_tab, ac[i], ac[i + 1]);
         }
         need = !(fmaxf(worst, worst_r) < 0.0f) || !rok;
         if (!need) ef_pack<M, N>(ac, rq, keep_a, keep_r, clamps, ca, cr);
