@@ -273,7 +273,10 @@ class DecodeWorkload:
                 self.gathered[i].copy_(gather_head_outputs(self.out[i], self.plan, self.group))
 
     def launches_per_step(self) -> int:
-        return self.L  # one fused decode launch per layer (split merge inside)
+        # one fused decode launch per layer (split merge inside); G = 8 from 16K
+        # tokens adds the separate split-merge launch (decode.cu launch_dq_path)
+        sep = self.G == 8 and self.T >= 16384 and self.peers is None
+        return self.L * (2 if sep else 1)
 
     def bytes_per_launch(self) -> int:
         return self.upl * unit_bytes(self.T, self.G, 128, self.m, self.n, self.value_bits)

@@ -201,6 +201,8 @@ int pqb_decode_attn(const pqb_cache* cache, int64_t n_units, int group, const vo
                                       the score rows, within 1e-4 max(1, peak) of qk_scores instead of
                                       bit-identical (no softmax, no value bytes)                       */
 #define PQB_DECODE_LUT 8           /* fused call: LUT-gather scoring (default for scores / G = 1)     */
+#define PQB_DECODE_MERGE_KERNEL 256 /* DQ fused call: split merge in a separate PDL launch instead of
+                                       the last CTA of each unit (default for G = 8 from 16K tokens) */
 #define PQB_DECODE_PROBE_MEM 64    /* diagnostics, m4n4 DQ only: stream tiles, skip all compute      */
 #define PQB_DECODE_PROBE_COMPUTE 128 /* diagnostics, m4n4 DQ only: compute on L2-resident tiles      */
 int pqb_decode_attn_ex(const pqb_cache* cache, int64_t n_units, int group, const void* q,

@@ -20,6 +20,7 @@ PQB_F32, PQB_BF16, PQB_F16 = 0, 1, 2
 PQB_VQ4 = 16  # pqb_store.value_dtype: 4-bit per-token value codes
 PQB_DECODE_FORCE_GENERIC, PQB_DECODE_NO_COMBINE, PQB_DECODE_DQ, PQB_DECODE_LUT = 1, 2, 4, 8
 PQB_DECODE_PROBE_MEM, PQB_DECODE_PROBE_COMPUTE = 64, 128
+PQB_DECODE_MERGE_KERNEL = 256
 
 c_i32, c_i64, c_u64, c_f32, c_f64, c_sz = (
     ctypes.c_int32,

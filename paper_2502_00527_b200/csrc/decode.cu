@@ -335,12 +335,65 @@ __global__ void __launch_bounds__(kNW * 32, 1)
   }
 }
 
-// Stand-alone merge of decode_fast_kernel partials (used when the in-kernel
-// merge is disabled, e.g. kernel-only timing followed by an explicit merge).
-__global__ void combine_split_kernel(EpiArgs ep, WorkSplit ws, int G) {
-  const int64_t unit = blockIdx.x;
+// Stand-alone split merge after a DQ launch that wrote partials only
+// (PQB_DECODE_MERGE_KERNEL): one CTA per (unit, query), thread = output
+// element, launched with programmatic dependent launch so its CTAs are
+// resident and waiting when the decode grid drains.  Same LSE merge as
+// merge_slots (one element per thread instead of G * 128 / nthreads).
+__global__ void __launch_bounds__(128) merge_split_kernel(EpiArgs ep, WorkSplit ws) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t unit = blockIdx.x / ep.group;
+  const int g = static_cast<int>(blockIdx.x - unit * ep.group), e = threadIdx.x;
   const int nseg = static_cast<int>(last_cta(ws, unit) - first_cta(ws, unit) + 1);
-  merge_slots(ep, unit, nseg, G, threadIdx.x, blockDim.x);
+  constexpr int kB = 8;
+  float mx = -INFINITY, L = 0.0f, O = 0.0f;
+  for (int s0 = 0; s0 < nseg; s0 += kB) {
+    float ms[kB], ls[kB], os[kB];
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      const bool ok = s0 + k < nseg;
+      const int64_t sl = (unit * ep.slots + min(s0 + k, nseg - 1)) * ep.group + g;
+      const float m = __ldcg(ep.part_ml + 2 * sl), l = __ldcg(ep.part_ml + 2 * sl + 1);
+      const float o = __ldcg(ep.part_o + sl * 128 + e);
+      ms[k] = ok ? m : -INFINITY;
+      ls[k] = ok ? l : 0.0f;
+      os[k] = ok ? o : 0.0f;
+    }
+    float bm = mx;
+#pragma unroll
+    for (int k = 0; k < kB; ++k) bm = fmaxf(bm, ms[k]);
+    if (bm == -INFINITY) continue;
+    const float r = exp2f(mx - bm);
+    L *= r;
+    O *= r;
+#pragma unroll
+    for (int k = 0; k < kB; ++k) {
+      if (ms[k] == -INFINITY) continue;
+      const float sc = exp2f(ms[k] - bm);
+      L = fmaf(ls[k], sc, L);
+      O = fmaf(os[k], sc, O);
+    }
+    mx = bm;
+  }
+  emit(ep, unit, g, e, O / L);
+}
+
+static int launch_merge_split(const EpiArgs& ep, const WorkSplit& ws, int64_t n_units, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(n_units * ep.group));
+  cfg.blockDim = dim3(128);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, merge_split_kernel, ep, ws) != cudaSuccess) {
+    set_error("merge_split launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return PQB_ECUDA;
+  }
+  return PQB_OK;
 }
 
 // ------------------------------------------------------------------ generic kernel
@@ -641,7 +694,18 @@ static int launch_dq_path(const DecodeArgs& a, cudaStream_t s, bool& handled) {
     handled = true;
     return rc;
   }
-  return launch_decode_dq(a, ep, ws, grid, s, handled);
+  // Partials only in the decode grid and the split merge in a separate PDL
+  // launch (one CTA per (unit, query), all in parallel) instead of the last
+  // CTA of each unit merging G x 128 outputs serially in the tail: G = 8 from
+  // 16K tokens (configs[3] launch +2.5%, scripts/g8_scaling.py; shorter or
+  // G = 4 launches measured equal or slightly slower), or PQB_DECODE_MERGE_KERNEL.
+  // Not with peer outputs (the decode grid publishes them).
+  const bool sep = ((a.flags & PQB_DECODE_MERGE_KERNEL) || (a.group == 8 && a.max_tokens >= 16384)) && ep.merge &&
+                   a.out != nullptr && a.peer == nullptr;
+  if (sep) ep.merge = false;
+  const int rc2 = launch_decode_dq(a, ep, ws, grid, s, handled);
+  if (rc2 != PQB_OK || !handled || !sep) return rc2;
+  return launch_merge_split(ep, ws, a.n_units, s);
 }
 
 template <int G, bool EXACT>

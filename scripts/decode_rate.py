@@ -19,6 +19,7 @@ for name, kw in [("g4", dict(batch=16, hq=32, hkv=8, m=4, n=4)), ("g8", dict(bat
                  ("m3n2", dict(batch=8, hq=32, hkv=8, m=3, n=2))]:
     T = 131072 if name == "m3n2" else 32768
     w = bench.DecodeWorkload(dev, layers=8, T=T, page_tokens=int(os.environ.get("PQB_PAGE", 128)), seed=0, **kw)
+    w.base_flags = int(os.environ.get("PQB_EXTRA_FLAGS", 0))  # A/B of launch variants
     run = w.capture(lambda: w.step(_lib.PQB_DECODE_NO_COMBINE))
     step = w.capture(w.step)
     a = w.bytes_per_launch()

@@ -17,6 +17,7 @@ res = {}
 for T in [int(t) for t in os.environ.get("PQB_TS", "4096,8192,16384,32768,65536").split(",")]:
     w = bench.DecodeWorkload(dev, layers=8, T=T, batch=32, hq=8, hkv=1, m=4, n=4,
                              page_tokens=int(os.environ.get("PQB_PAGE", 256)), seed=0)
+    w.base_flags = int(os.environ.get("PQB_EXTRA_FLAGS", 0))  # A/B of launch variants
     run = w.capture(lambda: w.step(_lib.PQB_DECODE_NO_COMBINE))
     step = w.capture(w.step)
     k = w.timed(run, 6, 2) / w.L

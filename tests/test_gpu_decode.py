@@ -481,3 +481,21 @@ def test_dq_scores_mode(m, n, G, T, res, page):
             tol = 1e-4 * max(1.0, float(np.abs(exact_rows[u, g]).max()))
             err = float(np.abs(fast[u, g] - exact_rows[u, g]).max())
             assert err <= tol, (u, g, err, tol)
+
+
+@pytest.mark.parametrize("G", [4, 8])
+@pytest.mark.parametrize("T", [70, 4096, 20000])
+def test_separate_merge_kernel_matches_in_kernel_merge(G, T):
+    """PQB_DECODE_MERGE_KERNEL (split merge in its own PDL launch) gives the
+    in-kernel merge's outputs bit for bit (same LSE sequence per element)."""
+    U = 5
+    keys = np.stack([po.synthetic_keys(T, 128, seed=900 + u) for u in range(U)])
+    rng = np.random.default_rng(T)
+    vals = torch.from_numpy(rng.standard_normal((U, T, 128)).astype(np.float32)).to(torch.bfloat16)
+    q = torch.from_numpy(rng.standard_normal((U, G, 128)).astype(np.float32)).cuda()
+    cache = pq.PolarKVCache(pq.QuantConfig(4, 4), U, 128, 0, capacity=T, value_dtype=torch.bfloat16)
+    cache.prefill(torch.from_numpy(keys).cuda(), vals.cuda())
+    for dt in (torch.float32, torch.bfloat16):
+        a = cache.decode(q, out_dtype=dt)
+        b = cache.decode(q, out_dtype=dt, flags=pq._lib.PQB_DECODE_MERGE_KERNEL)
+        assert torch.equal(a, b)
