@@ -275,8 +275,9 @@ class DecodeWorkload:
     def launches_per_step(self) -> int:
         # one fused decode launch per layer (split merge inside); G = 8 from 16K
         # tokens adds the separate split-merge launch (decode.cu launch_dq_path)
+        # with the fused peer gather, one pqb_peer_wait launch per layer as well
         sep = self.G == 8 and self.T >= 16384 and self.peers is None
-        return self.L * (2 if sep else 1)
+        return self.L * (2 if sep or self.peers is not None else 1)
 
     def bytes_per_launch(self) -> int:
         return self.upl * unit_bytes(self.T, self.G, 128, self.m, self.n, self.value_bits)
@@ -309,7 +310,8 @@ class DecodeWorkload:
         torch.cuda.synchronize(self.dev)
         ms = e0.elapsed_time(e1) / steps
         if dist:
-            t = torch.tensor([ms], device=self.dev, dtype=torch.float64)
+            on_dev = dist.get_backend() == "nccl"
+            t = torch.tensor([ms], device=self.dev if on_dev else "cpu", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
@@ -340,7 +342,7 @@ def run_ours(a, rank: int, world: int, dist) -> dict | None:
 
     from paper_2502_00527_b200 import sharding
 
-    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    dev = torch.device("cuda", torch.cuda.current_device() if world > 1 else int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     G = a.hq // a.hkv
     plan = None
@@ -578,8 +580,11 @@ def main() -> None:
         import torch
         import torch.distributed as tdist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        tdist.init_process_group("nccl")
+        # PQB_BENCH_DEVICE / PQB_BENCH_BACKEND: run the N > 1 path as N ranks on
+        # one GPU over gloo (a smoke test of the multi-rank code on a 1-GPU box)
+        dev_override = os.environ.get("PQB_BENCH_DEVICE")
+        torch.cuda.set_device(int(dev_override) if dev_override is not None else int(os.environ.get("LOCAL_RANK", 0)))
+        tdist.init_process_group(os.environ.get("PQB_BENCH_BACKEND", "nccl"))
         dist = tdist
     G = a.hq // a.hkv
     upl = a.batch * a.hkv
