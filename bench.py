@@ -273,11 +273,14 @@ class DecodeWorkload:
                 self.gathered[i].copy_(gather_head_outputs(self.out[i], self.plan, self.group))
 
     def launches_per_step(self) -> int:
-        # one fused decode launch per layer (split merge inside); G = 8 from 16K
-        # tokens adds the separate split-merge launch (decode.cu launch_dq_path)
-        # with the fused peer gather, one pqb_peer_wait launch per layer as well
-        sep = self.G == 8 and self.T >= 16384 and self.peers is None
-        return self.L * (2 if sep or self.peers is not None else 1)
+        # per layer: the fused decode, plus the separate split-merge launch when
+        # the library picks it for this shape (pqb_decode_launches), or with the
+        # fused peer gather the pqb_peer_wait launch (the merge stays in-kernel)
+        from paper_2502_00527_b200 import _lib
+
+        if self.peers is not None:
+            return 2 * self.L
+        return self.L * int(_lib.load().pqb_decode_launches(self.upl, self.G, self.T, self.base_flags))
 
     def bytes_per_launch(self) -> int:
         return self.upl * unit_bytes(self.T, self.G, 128, self.m, self.n, self.value_bits)

@@ -202,7 +202,8 @@ int pqb_decode_attn(const pqb_cache* cache, int64_t n_units, int group, const vo
                                       bit-identical (no softmax, no value bytes)                       */
 #define PQB_DECODE_LUT 8           /* fused call: LUT-gather scoring (default for scores / G = 1)     */
 #define PQB_DECODE_MERGE_KERNEL 256 /* DQ fused call: split merge in a separate PDL launch instead of
-                                       the last CTA of each unit (default for G = 8 from 16K tokens) */
+                                       the last CTA of each unit (default for G = 8 from 16K tokens and
+                                       when units are cut into more than 8 segments)                 */
 #define PQB_DECODE_PROBE_MEM 64    /* diagnostics, m4n4 DQ only: stream tiles, skip all compute      */
 #define PQB_DECODE_PROBE_COMPUTE 128 /* diagnostics, m4n4 DQ only: compute on L2-resident tiles      */
 int pqb_decode_attn_ex(const pqb_cache* cache, int64_t n_units, int group, const void* q,
@@ -239,6 +240,9 @@ int pqb_decode_attn_peer(const pqb_cache* cache, int64_t n_units, int group, con
 int pqb_peer_wait(const uint32_t* flags, int n_peers, int rank, uint32_t* expect, pqb_stream_t stream);
 
 int pqb_decode_splits(int64_t n_units, int max_tokens);
+/* Kernels one fused DQ decode call (group 4 or 8, out != NULL, no peers) enqueues
+ * for this shape and flags: 1, or 2 when the split merge runs as its own launch. */
+int pqb_decode_launches(int64_t n_units, int group, int max_tokens, int flags);
 
 /* ------------------------------------------------------------ accessors ----
  * Tables and views the reference API exposes (all computed on the device). */

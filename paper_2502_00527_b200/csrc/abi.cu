@@ -255,6 +255,11 @@ int pqb_peer_wait(const uint32_t* flags, int n_peers, int rank, uint32_t* expect
   return cuda_status("pqb_peer_wait");
 }
 
+int pqb_decode_launches(int64_t n_units, int group, int max_tokens, int flags) {
+  if (n_units <= 0 || max_tokens <= 0) return 1;
+  return decode_launch_count(n_units, group, max_tokens, flags);
+}
+
 int pqb_decode_splits(int64_t n_units, int max_tokens) {
   if (n_units <= 0 || max_tokens <= 0) return 1;
   return decode_splits(n_units, max_tokens);

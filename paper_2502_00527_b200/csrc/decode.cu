@@ -685,6 +685,24 @@ static bool use_dq(const DecodeArgs& a) {
   return true;
 }
 
+// Partials only in the decode grid and the split merge in a separate PDL launch
+// (one CTA per (unit, query), all in parallel) instead of the last CTA of each
+// unit merging G x 128 outputs serially in the launch's tail, when units are
+// cut into many segments (> 8: configs[0] 11.8 -> 9.8 us per launch,
+// profiles/r01/small_launch.md) or for G = 8 from 16K tokens (configs[3] +2.5%,
+// scripts/g8_scaling.py); G = 4 long launches and short G = 8 ones measured
+// equal or slightly slower.  PQB_DECODE_MERGE_KERNEL forces it.
+static bool separate_merge(int flags, int group, int max_tokens, const WorkSplit& ws) {
+  const int64_t seg_max = (ws.tiles_max + ws.per_cta - 1) / ws.per_cta + 1;
+  return (flags & PQB_DECODE_MERGE_KERNEL) || seg_max > 8 || (group == 8 && max_tokens >= 16384);
+}
+
+int decode_launch_count(int64_t n_units, int group, int max_tokens, int flags) {
+  if (group != 4 && group != 8) return 1;
+  const WorkSplit ws = make_split(n_units, max_tokens, std::min(num_sms(), kMaxCtas));
+  return (flags & PQB_DECODE_NO_COMBINE) || !separate_merge(flags, group, max_tokens, ws) ? 1 : 2;
+}
+
 static int launch_dq_path(const DecodeArgs& a, cudaStream_t s, bool& handled) {
   EpiArgs ep;
   WorkSplit ws;
@@ -694,14 +712,8 @@ static int launch_dq_path(const DecodeArgs& a, cudaStream_t s, bool& handled) {
     handled = true;
     return rc;
   }
-  // Partials only in the decode grid and the split merge in a separate PDL
-  // launch (one CTA per (unit, query), all in parallel) instead of the last
-  // CTA of each unit merging G x 128 outputs serially in the tail: G = 8 from
-  // 16K tokens (configs[3] launch +2.5%, scripts/g8_scaling.py; shorter or
-  // G = 4 launches measured equal or slightly slower), or PQB_DECODE_MERGE_KERNEL.
-  // Not with peer outputs (the decode grid publishes them).
-  const bool sep = ((a.flags & PQB_DECODE_MERGE_KERNEL) || (a.group == 8 && a.max_tokens >= 16384)) && ep.merge &&
-                   a.out != nullptr && a.peer == nullptr;
+  const bool sep = ep.merge && a.out != nullptr && a.peer == nullptr &&
+                   separate_merge(a.flags, a.group, a.max_tokens, ws);
   if (sep) ep.merge = false;
   const int rc2 = launch_decode_dq(a, ep, ws, grid, s, handled);
   if (rc2 != PQB_OK || !handled || !sep) return rc2;
