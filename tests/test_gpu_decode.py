@@ -499,3 +499,17 @@ def test_separate_merge_kernel_matches_in_kernel_merge(G, T):
         a = cache.decode(q, out_dtype=dt)
         b = cache.decode(q, out_dtype=dt, flags=pq._lib.PQB_DECODE_MERGE_KERNEL)
         assert torch.equal(a, b)
+
+
+def test_decode_launch_count_policy():
+    """pqb_decode_launches: the split merge gets its own launch for G = 8 from
+    16K tokens and whenever units span more than 8 segments, never with
+    NO_COMBINE; a merge-kernel shape still decodes to the LUT path's outputs."""
+    lib = pq._lib.load()
+    assert lib.pqb_decode_launches(128, 4, 32768, 0) == 1  # configs[1] layer
+    assert lib.pqb_decode_launches(8, 4, 4096, 0) == 2  # configs[0]: 16+ segments per unit
+    assert lib.pqb_decode_launches(32, 8, 32768, 0) == 2  # configs[3] layer
+    assert lib.pqb_decode_launches(32, 8, 4096, 0) == 1
+    assert lib.pqb_decode_launches(128, 4, 32768, pq._lib.PQB_DECODE_MERGE_KERNEL) == 2
+    assert lib.pqb_decode_launches(8, 4, 4096, pq._lib.PQB_DECODE_NO_COMBINE) == 1
+    assert lib.pqb_decode_launches(8, 1, 4096, 0) == 1  # LUT kernel: merge in-kernel
