@@ -52,11 +52,20 @@ namespace pqb {
 // Warp specialisation: a fourth warpgroup of producers (warp kNW + j fills the
 // rings of compute warps j and j + 4, which share its SM sub-partition) takes
 // the TMA issue code off the compute warps; registers are rebalanced with
-// setmaxnreg (compute warps 240, producers 32: 2 x 128 x 240 + 128 x 32 = 64K).
+// setmaxnreg (compute warps 232, producers 40: 2 x 128 x 232 + 128 x 40 <= 64K).
 // PQB_DQ_WS=0 builds the previous layout (lane 0 of each compute warp issues).
 #ifndef PQB_DQ_WS
 #define PQB_DQ_WS 1
 #endif
+#ifndef PQB_DQ_CONS_REGS
+#define PQB_DQ_CONS_REGS 232
+#define PQB_DQ_PROD_REGS 40
+#endif
+// setmaxnreg.inc blocks until the CTA's own pool (168 x 384 allocated at launch)
+// has the registers the producers released: two compute warpgroups may grow by
+// no more than the producer warpgroup shrinks, or the kernel deadlocks (240/32
+// does: 2 x 72 > 136).
+static_assert(2 * (PQB_DQ_CONS_REGS - 168) <= 168 - PQB_DQ_PROD_REGS, "setmaxnreg budget exceeds the CTA pool");
 constexpr bool kDqWs = PQB_DQ_WS != 0;
 constexpr int kDqThreads = kDqWs ? (kNW + 4) * 32 : kNW * 32;
 constexpr int kConsThreads = kNW * 32;
@@ -308,7 +317,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 
   if constexpr (kDqWs) {
     if (warp >= kNW) {  // ---- producer warpgroup
-      asm volatile("setmaxnreg.dec.sync.aligned.u32 40;" ::: "memory");
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PQB_DQ_PROD_REGS) : "memory");
       const int w0 = warp - kNW, w1 = w0 + 4;
       uint32_t it0 = 0, it1 = 0;
       bool first_seg = true;
@@ -348,7 +357,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       if (!first_seg) named_sync(2, kDqThreads);
       return;
     }
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(PQB_DQ_CONS_REGS) : "memory");
   }
 
   const int g8 = lane >> 2, t4 = lane & 3;  // fragment group / thread-in-group
