@@ -180,6 +180,19 @@ def _cpu_worker(args):
             return done, el
 
 
+def cpu_model() -> str:
+    """The host CPU (state the core count and the lscpu model)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline(T, d, m, n, G, units_per_step, batch, seconds: float) -> dict:
     """Reference CPU path on every host core (one process per core) for
     ~``seconds`` of decode work each, extrapolated linearly to a full step."""
@@ -198,6 +211,7 @@ def cpu_baseline(T, d, m, n, G, units_per_step, batch, seconds: float) -> dict:
         "value": batch / step_s,
         "unit": "tokens/s",
         "cores": cores,
+        "cpu_model": cpu_model(),
         "kind": "port",
         "sample": f"{n_units} unit-decodes ({G} query heads each, T={T}: qk_scores + attention_weights + "
                   f"softmax.V of the numpy oracle port of the reference) on {cores} processes, {wall:.1f}s wall "
