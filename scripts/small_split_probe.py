@@ -19,4 +19,14 @@ for ctas in (0, 16, 32, 48, 64, 96, 128):
             w.views[i].decode(w.q[i], out=w.out[i], max_tokens=w.T, splits=ctas)
     g = w.capture(step)
     res[ctas] = [round(w.timed(g, 50, 5) / w.L * 1e3, 2) for _ in range(2)]
+from paper_2502_00527_b200 import _lib
+
+
+def step_mk():
+    for i in range(w.L):
+        w.views[i].decode(w.q[i], out=w.out[i], max_tokens=w.T, flags=_lib.PQB_DECODE_MERGE_KERNEL)
+
+
+g = w.capture(step_mk)
+res["default+merge_kernel"] = [round(w.timed(g, 50, 5) / w.L * 1e3, 2) for _ in range(2)]
 print(json.dumps({"us_per_launch_by_ctas": res}))
