@@ -22,7 +22,15 @@ dev = torch.device("cuda", 0)
 w = bench.DecodeWorkload(dev, layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, page_tokens=int(os.environ.get("PQB_PAGE", 256)), seed=0,
                          value_bits=vbits)
 algo = w.bytes_per_launch()
-run = w.capture(lambda: w.step(_lib.PQB_DECODE_NO_COMBINE | flags))
+spl = int(os.environ.get("PQB_SPLITS", 0))  # CTA count handed to the split (0: one per SM)
+
+
+def step_s(f):
+    for i in range(w.L):
+        w.views[i].decode(w.q[i], out=w.out[i], max_tokens=w.T, flags=f, splits=spl)
+
+
+run = w.capture(lambda: step_s(_lib.PQB_DECODE_NO_COMBINE | flags))
 Path("gpurun_out").mkdir(exist_ok=True)
 smi = subprocess.Popen(
     ["nvidia-smi", "--query-gpu=timestamp,clocks.sm,clocks.mem,power.draw,temperature.gpu,temperature.memory,"
@@ -42,6 +50,6 @@ for _ in range(3):
     idle_after.append(round(algo / (ms * 1e-3) / 1e9 / 6546.9, 3))
 smi.terminate()
 step_ms = w.timed(w.capture(w.step), 10, 2)
-print(json.dumps({"flags": flags, "value_bits": vbits, "lib": os.environ.get("PQB_LIB", ""),
+print(json.dumps({"flags": flags, "value_bits": vbits, "lib": os.environ.get("PQB_LIB", ""), "splits": spl,
                   "median_last_half": statistics.median(rates[len(rates) // 2:]), "chunk_rates": rates, "after_2s_idle": idle_after,
                   "tokens_per_s_cool": round(w.batch / (step_ms * 1e-3), 1)}))
