@@ -57,6 +57,10 @@ namespace pqb {
 #ifndef PQB_DQ_WS
 #define PQB_DQ_WS 1
 #endif
+// the product-table layout (see kPtTabAbs below); before DqCfg, which sizes by it
+#ifndef PQB_DQ_PRMT_TAB
+#define PQB_DQ_PRMT_TAB 1
+#endif
 #ifndef PQB_DQ_CONS_REGS
 #define PQB_DQ_CONS_REGS 232
 #define PQB_DQ_PROD_REGS 40
@@ -83,13 +87,36 @@ struct DqCfg {
   static constexpr int kFragBytes = 16 * 32 * 16;            // Q' A-fragments [ks][lane] uint4 (hi, lo, hi, lo)
   static constexpr int kHeadBytes = kTabBytes + kFragBytes + G * 128 * 4 + 128 + 8 * (1 << M);
   static constexpr int kWarpBytes = kStages * kStageBytes + kPBytes;
+#if PQB_DQ_PRMT_TAB
+  // the whole opt-in budget minus the 256 B of static barriers; the kernel
+  // checks that its stages fit around the table
+  static constexpr int kSmem = 232448 - 256;
+#else
   static constexpr int kSmem = kHeadBytes + kNW * kWarpBytes + 128;
+#endif
   static constexpr bool kPacked = G <= 4;  // P.V: columns 0-3 carry P_hi, 4-7 P_lo
   static_assert(kHeadBytes % 16 == 0 && kWarpBytes % 16 == 0, "alignment");
   static_assert(kNW * kStages * kStageBytes >= kNW * G * 132 * 4, "merge area");
 };
 
 PQB_DEV uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// PQB_DQ_PRMT_TAB=1 (default; A/B +1.3% G = 4, +2.9% G = 8, all decode tests
+// green; 0 builds the previous layout): the product table sits at shared-window
+// address 0x10000 in 256 slots of 256 B (slot e's first 128 B = entry e's 16
+// bank-slot copies), so one PRMT composes a gather address from the index
+// byte, the lane's copy offset and the table base (no add); the slots' second
+// halves hold the small buffers (GapArr), the stages sit before and after the
+// table (scripts/micro/smem_base.cu: 1 KB reserved, static from 0x400).
+constexpr uint32_t kPtTabAbs = 0x10000;
+template <typename T>
+struct GapArr {
+  static constexpr int kPer = 128 / sizeof(T);
+  uint8_t* tab;
+  int g0;
+  PQB_DEV T& operator[](int i) const { return reinterpret_cast<T*>(tab + (g0 + i / kPer) * 256 + 128)[i % kPer]; }
+};
+constexpr int kGapQfrag = 0, kGapQ = 64, kGapRbuf = 96, kGapMisc = 160, kGapCs = 161, kGapScale = 162;
 
 PQB_DEV void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -170,8 +197,14 @@ struct DqIdx {
   }
   // shared address of the k-step ks entry in the lane's table copy
   PQB_DEV uint32_t addr(uint32_t tab, int ks) const {
+#if PQB_DQ_PRMT_TAB
+    // tab = kPtTabAbs | lane copy offset: the absolute address in one PRMT
+    if constexpr (kFused) return __byte_perm(w[ks >> 2], tab, 0x7604u | ((ks & 3) << 4));
+    else return tab + (w[ks] << 8);
+#else
     if constexpr (kFused) return tab + (__byte_perm(w[ks >> 2], 0u, 0x4440u | (ks & 3)) << 7);
     else return tab + (w[ks] << 7);
+#endif
   }
 };
 
@@ -255,22 +288,46 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   constexpr bool kPacked = Cfg::kPacked;
   static_assert(G == 1 || G == 2 || G == 4 || G == 8, "G");
   extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#if PQB_DQ_PRMT_TAB
+  const int tab_off = static_cast<int>(kPtTabAbs - smem_u32(smem));  // dynamic offset of the table
+  const int n_before = tab_off / Cfg::kStageBytes;                     // stages before the table
+  uint8_t* const tabp = smem + tab_off;
+  uint2* ptab = reinterpret_cast<uint2*>(tabp);  // entry e at slot e (e * 32 uint2)
+  const GapArr<uint4> qfrag{tabp, kGapQfrag};
+  const GapArr<float> q_s{tabp, kGapQ};
+  int* s_misc = reinterpret_cast<int*>(tabp + kGapMisc * 256 + 128);
+  float2* cs_s = reinterpret_cast<float2*>(tabp + kGapCs * 256 + 128);
+  const GapArr<float> s_scale{tabp, kGapScale};  // 64 floats: two gaps
+  auto stage_ptr = [&](int i) -> uint8_t* {
+    return smem + (i < n_before ? i * Cfg::kStageBytes : tab_off + 65536 + (i - n_before) * Cfg::kStageBytes);
+  };
+  uint8_t* warp_area = smem;  // merge scratch aliases the first stages (all before the table)
+  if (tid == 0 && (tab_off < 0 || n_before * Cfg::kStageBytes < kNW * G * 132 * 4 ||
+                   tab_off + 65536 + (kNW * kStages - n_before) * Cfg::kStageBytes > Cfg::kSmem))
+    __trap();  // shared-window layout other than measured: the table cannot sit at kPtTabAbs
+  const GapArr<float> rbuf{tabp, kGapRbuf + 8 * (warp < kNW ? warp : 0)};
+#else
   uint2* ptab = reinterpret_cast<uint2*>(smem);                                   // [2^(M+N)][16]
   uint4* qfrag = reinterpret_cast<uint4*>(smem + Cfg::kTabBytes);                    // [16][32]
   float* q_s = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(qfrag) + Cfg::kFragBytes);  // [G][128]
   int* s_misc = reinterpret_cast<int*>(q_s + G * 128);  // [0] max|Q'| bits, [1] merge flag
   float2* cs_s = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(s_misc) + 128);  // [2^M] (cos, sin)
   uint8_t* warp_area = smem + Cfg::kHeadBytes;
-
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint8_t* my_area = warp_area + warp * Cfg::kWarpBytes;
-  float* rbuf = reinterpret_cast<float*>(my_area + kStages * Cfg::kStageBytes);  // [32][8]
+  auto stage_ptr = [&](int i) -> uint8_t* {
+    return warp_area + (i / kStages) * Cfg::kWarpBytes + (i % kStages) * Cfg::kStageBytes;
+  };
+  float* rbuf = reinterpret_cast<float*>(warp_area + (warp < kNW ? warp : 0) * Cfg::kWarpBytes +
+                                         kStages * Cfg::kStageBytes);  // [32][8]
+#endif
   // mbarriers live outside the warp areas: the end-of-segment merge scratch
   // (red, G * 132 floats per warp) aliases the stage memory and, at G = 8,
   // would run over warp 0's barriers if they sat behind its stages
   __shared__ uint64_t s_bar[kNW][kStages];    // stage full (TMA transaction count)
   __shared__ uint64_t s_empty[kNW][kStages];  // stage released by its compute warp (WS)
-  __shared__ float s_scale[64];               // the current unit's radius scales
+#if !PQB_DQ_PRMT_TAB
+  __shared__ float s_scale[64];  // the current unit's radius scales
+#endif
   uint64_t* bar = s_bar[warp < kNW ? warp : 0];
   if (lane == 0 && warp < kNW) {
 #pragma unroll
@@ -297,12 +354,16 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     const uint32_t hi = h2_bits(__halves2half2(xh, yh));
     const uint32_t lo = h2_bits(__halves2half2(__float2half_rn(static_cast<float>(x - __half2float(xh))),
                                                __float2half_rn(static_cast<float>(y - __half2float(yh)))));
-    uint4* dst = reinterpret_cast<uint4*>(ptab + e * 16);
+    uint4* dst = reinterpret_cast<uint4*>(ptab + e * (PQB_DQ_PRMT_TAB ? 32 : 16));
 #pragma unroll
     for (int k = 0; k < 8; ++k) dst[k] = make_uint4(hi, lo, hi, lo);
   }
   if constexpr (kDqWs) __syncthreads();  // producers helped build the table
+#if PQB_DQ_PRMT_TAB
+  const uint32_t ptab_l = kPtTabAbs | ((lane & 15) << 3);  // this lane's bank-slot copy
+#else
   const uint32_t ptab_l = smem_u32(smem) + ((lane & 15) << 3);  // this lane's bank-slot copy
+#endif
   // Programmatic dependent launch: everything above uses constants only; the
   // cache, q and the outputs may belong to the previous kernel in the stream.
   // Let the next launch start its own prologue as SMs drain, then wait for
@@ -339,7 +400,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             const uint32_t s = it % kStages;
             mbar_wait(&s_empty[w][s], ((it / kStages) & 1) ^ 1);
             fence_proxy_async_smem();
-            issue_tile_dq<M, N, VQ, kScores>(warp_area + w * Cfg::kWarpBytes + s * Cfg::kStageBytes, c.store,
+            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(w * kStages + s), c.store,
                                     page_base_c(c.store, unit, PROBE == 2 ? 0 : cu.pg), PROBE == 2 ? 0 : cu.tin,
                                     &s_bar[w][s]);
           };
@@ -448,7 +509,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         if (cur.tile < t_hi) {
           fence_proxy_async_smem();
           const uint32_t sl = (k_iter + s) % kStages;
-          issue_tile_dq<M, N, VQ, kScores>(my_area + sl * Cfg::kStageBytes, c.store,
+          issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kStages + sl), c.store,
                                   page_base_c(c.store, unit, PROBE == 2 ? 0 : cur.pg), PROBE == 2 ? 0 : cur.tin,
                                   bar + sl);
         }
@@ -468,7 +529,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       const uint32_t s = k_iter % kStages;
       const int nt = tile + kStages * kNW;  // the tile this stage is refilled with
       mbar_wait(bar + s, (k_iter / kStages) & 1);
-      const uint8_t* st = my_area + s * Cfg::kStageBytes;
+      const uint8_t* st = stage_ptr(warp * kStages + s);
       const int tok0 = tile * kTile;
       if constexpr (PROBE == 1) {
         __syncwarp();
@@ -477,7 +538,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         } else if (lane == 0) {
           if (nt < t_hi) {
             fence_proxy_async_smem();
-            issue_tile_dq<M, N, VQ, kScores>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, cur.pg), cur.tin,
+            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kStages + s), c.store, page_base_c(c.store, unit, cur.pg), cur.tin,
                                     bar + s);
           }
           cur.next(dpg, dtin, tpp);
@@ -577,7 +638,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         } else if (lane == 0) {
           if (nt < t_hi) {
             fence_proxy_async_smem();
-            issue_tile_dq<M, N, VQ, kScores>(my_area + s * Cfg::kStageBytes, c.store, page_base_c(c.store, unit, cur.pg),
+            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kStages + s), c.store, page_base_c(c.store, unit, cur.pg),
                                              cur.tin, bar + s);
           }
           cur.next(dpg, dtin, tpp);
@@ -684,7 +745,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       } else if (lane == 0) {
         if (nt < t_hi) {
           fence_proxy_async_smem();
-          issue_tile_dq<M, N, VQ, kScores>(my_area + s * Cfg::kStageBytes, c.store,
+          issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kStages + s), c.store,
                                   page_base_c(c.store, unit, PROBE == 2 ? 0 : cur.pg), PROBE == 2 ? 0 : cur.tin,
                                   bar + s);
         }
@@ -752,6 +813,31 @@ static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws
   using Cfg = DqCfg<G, M, N, VQ>;
   static bool attr_set = false;
   if (!attr_set) {
+#if PQB_DQ_PRMT_TAB
+    {  // the table must land at kPtTabAbs with the stages around it (as the kernel assumes)
+      cudaFuncAttributes fa;
+      int dev = 0, reserved = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+      if (cudaFuncGetAttributes(&fa, decode_dq_kernel<G, M, N, PROBE, VQ>) != cudaSuccess) {
+        set_error("cudaFuncGetAttributes failed");
+        return PQB_ECUDA;
+      }
+      // static bytes as reported may include the reserved block; dynamic memory starts after both
+      const int stat = static_cast<int>(fa.sharedSizeBytes) >= reserved ? static_cast<int>(fa.sharedSizeBytes) - reserved
+                                                                         : static_cast<int>(fa.sharedSizeBytes);
+      const int dyn0 = reserved + ((stat + 127) / 128) * 128;
+      const int tab_off = static_cast<int>(kPtTabAbs) - dyn0;
+      const int n_before = tab_off / Cfg::kStageBytes;
+      if (tab_off < 0 || n_before * Cfg::kStageBytes < kNW * G * 132 * 4 ||
+          tab_off + 65536 + (kNW * kStages - n_before) * Cfg::kStageBytes > Cfg::kSmem ||
+          stat + Cfg::kSmem > 232448) {
+        set_error("decode_dq: shared-window layout (reserved %d, static %d) leaves no room for the table at 0x%x",
+                  reserved, stat, kPtTabAbs);
+        return PQB_ECUDA;
+      }
+    }
+#endif
     if (cudaFuncSetAttribute(decode_dq_kernel<G, M, N, PROBE, VQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg::kSmem) != cudaSuccess) {
       set_error("cudaFuncSetAttribute(smem=%d) failed", Cfg::kSmem);
