@@ -128,10 +128,13 @@ PQB_DEV void mma_f16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint3
 
 // Lane t4 owns channel pairs [16 t4, 16 t4 + 16) of every token; k-step ks
 // contracts pair 16 t4 + dq_pair(ks).  For m = n = 4 the order follows the
-// nibble fusion below (even pairs of a word, then odd), else it is ks.
-template <bool FUSED>
+// nibble fusion below (even pairs of a word, then odd); for m = 3, n = 2 the
+// SWAR byte spread (byte b of word j = pair 4b + j, k-step 4j + b); else ks.
+template <int M, int N>
 PQB_DEV constexpr int dq_pair(int ks) {
-  return FUSED ? ((ks >> 2) & 1) + 2 * (ks & 3) + 8 * (ks >> 3) : ks;
+  return (M == 4 && N == 4) ? ((ks >> 2) & 1) + 2 * (ks & 3) + 8 * (ks >> 3)
+         : (M == 3 && N == 2 && PQB_DQ_PRMT_TAB) ? 4 * (ks & 3) + (ks >> 2)
+                                                 : ks;
 }
 
 // B bits starting at bit b of the little-endian word array x (b compile-time
@@ -173,7 +176,8 @@ PQB_DEV void load_lane_codes(const uint8_t* row, int t4, uint32_t (&x)[(B + 1) /
 template <int M, int N>
 struct DqIdx {
   static constexpr bool kFused = M == 4 && N == 4;
-  uint32_t w[kFused ? 4 : 16];
+  static constexpr bool kSwar = M == 3 && N == 2 && PQB_DQ_PRMT_TAB;  // byte-spread indices, PRMT addressing
+  uint32_t w[kFused || kSwar ? 4 : 16];
   PQB_DEV void load(const uint8_t* arow, const uint8_t* rrow, int t4, bool live) {
     if constexpr (kFused) {
       const uint2 a = *reinterpret_cast<const uint2*>(arow + 8 * t4);
@@ -183,6 +187,26 @@ struct DqIdx {
       w[1] = (a.x & 0xF0F0F0F0u) | ((r.x >> 4) & 0x0F0F0F0Fu);
       w[2] = ((a.y << 4) & 0xF0F0F0F0u) | (r.y & 0x0F0F0F0Fu);
       w[3] = (a.y & 0xF0F0F0F0u) | ((r.y >> 4) & 0x0F0F0F0Fu);
+    } else if constexpr (kSwar) {
+      // 16 pairs: angle a_k at bits 3k of 48, radius r_k at bits 2k of 32; byte b
+      // of w[j] = (a_{4b+j} << 2) | r_{4b+j}
+      uint32_t xa[3];
+      load_lane_codes<3>(arow, t4, xa);  // bits 0..47 valid (xa[1] bits 16+ belong to the next lane)
+      uint32_t R = reinterpret_cast<const uint32_t*>(rrow)[t4];
+      if (!live) R = 0u;
+      const uint32_t E = R & 0x33333333u, O = (R >> 2) & 0x33333333u;  // r_{2i} / r_{2i+1} in nibble i
+      const uint32_t rw[4] = {E & 0x0F0F0F0Fu, O & 0x0F0F0F0Fu, (E >> 4) & 0x0F0F0F0Fu, (O >> 4) & 0x0F0F0F0Fu};
+      // 12-bit groups g_b = a_{4b..4b+3}: P0 = g0 | g2 << 16, P1 = g1 | g3 << 16 (stray
+      // bits land at 12-15 / 28-31, outside every field mask below)
+      const uint32_t t24 = __funnelshift_r(xa[0], xa[1], 24);
+      const uint32_t P0 = (xa[0] & 0xFFFu) | ((t24 << 16) & 0x0FFF0000u);
+      const uint32_t P1 = ((xa[0] >> 12) & 0xFFFu) | ((xa[1] << 12) & 0x0FFF0000u);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t lo = (P0 >> (3 * j)) & 0x00070007u;                                   // bytes 0, 2
+        const uint32_t hi = (j < 3 ? (P1 << (8 - 3 * j)) : (P1 >> 1)) & 0x07000700u;        // bytes 1, 3
+        w[j] = ((lo | hi) << 2) | rw[j];
+      }
     } else {
       uint32_t xa[(M + 1) / 2 + 1], xr[(N + 1) / 2 + 1];
       load_lane_codes<M>(arow, t4, xa);
@@ -199,7 +223,7 @@ struct DqIdx {
   PQB_DEV uint32_t addr(uint32_t tab, int ks) const {
 #if PQB_DQ_PRMT_TAB
     // tab = kPtTabAbs | lane copy offset: the absolute address in one PRMT
-    if constexpr (kFused) return __byte_perm(w[ks >> 2], tab, 0x7604u | ((ks & 3) << 4));
+    if constexpr (kFused || kSwar) return __byte_perm(w[ks >> 2], tab, 0x7604u | ((ks & 3) << 4));
     else return tab + (w[ks] << 8);
 #else
     if constexpr (kFused) return tab + (__byte_perm(w[ks >> 2], 0u, 0x4440u | (ks & 3)) << 7);
@@ -475,7 +499,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       const int ks = i >> 5, ln = i & 31, g = ln >> 2, t = ln & 3;
       uint4 v = make_uint4(0u, 0u, 0u, 0u);
       if (g < G) {
-        const int j = 16 * t + dq_pair<kFused>(ks);
+        const int j = 16 * t + dq_pair<M, N>(ks);
         const float sj = s_scale[j];
         const int ex = c.layout == PQB_HALF_SPLIT ? j : 2 * j;
         const int ey = c.layout == PQB_HALF_SPLIT ? j + 64 : 2 * j + 1;
