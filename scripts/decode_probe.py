@@ -13,9 +13,10 @@ import bench
 
 vb = int(sys.argv[1]) if len(sys.argv) > 1 else 0
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 2
-shape = dict(batch=32, hq=8, hkv=1) if (sys.argv[3] if len(sys.argv) > 3 else "g4") == "g8" else dict(
-    batch=16, hq=32, hkv=8)
-w = bench.DecodeWorkload(torch.device("cuda", 0), layers=L, T=int(os.environ.get("PQB_T", 32768)), m=4, n=4,
+kind = sys.argv[3] if len(sys.argv) > 3 else "g4"
+shape = {"g8": dict(batch=32, hq=8, hkv=1), "m3n2": dict(batch=8, hq=32, hkv=8)}.get(kind, dict(batch=16, hq=32, hkv=8))
+m, n, T = (3, 2, 131072) if kind == "m3n2" else (4, 4, 32768)  # m3n2: the configs[2] launch
+w = bench.DecodeWorkload(torch.device("cuda", 0), layers=L, T=int(os.environ.get("PQB_T", T)), m=m, n=n,
                          page_tokens=int(os.environ.get("PQB_PAGE", 256)), seed=0, value_bits=vb or None, **shape)
 for _ in range(3):
     w.step()
