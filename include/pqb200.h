@@ -60,6 +60,7 @@ extern "C" {
 #define PQB_F32 0
 #define PQB_BF16 1
 #define PQB_F16 2
+#define PQB_F64 3 /* element-wise reference API only (to_polar / quantize_angle / quantize_radius) */
 /* pqb_store.value_dtype only: 4-bit per-token uniform value codes
  * (quantize_uniform PER_TOKEN, baseline_quant.py:58-110; the reference's
  * PackedKVCache(quantize_values=True, value_bits=4), kv_cache.py:199-209).
@@ -204,6 +205,8 @@ int pqb_decode_attn(const pqb_cache* cache, int64_t n_units, int group, const vo
 #define PQB_DECODE_MERGE_KERNEL 256 /* DQ fused call: split merge in a separate PDL launch instead of
                                        the last CTA of each unit (default for G = 8 from 16K tokens and
                                        when units are cut into more than 8 segments)                 */
+#define PQB_DECODE_DQ_LINEAR 512   /* DQ kernel: the linear shared-memory layout build (the automatic
+                                       fallback when the default table placement does not fit)        */
 #define PQB_DECODE_PROBE_MEM 64    /* diagnostics, m4n4 DQ only: stream tiles, skip all compute      */
 #define PQB_DECODE_PROBE_COMPUTE 128 /* diagnostics, m4n4 DQ only: compute on L2-resident tiles      */
 int pqb_decode_attn_ex(const pqb_cache* cache, int64_t n_units, int group, const void* q,
@@ -282,6 +285,37 @@ int pqb_quantize_values(const void* values, int dtype, int64_t n, int d, int bit
 /* attention_weights (lut_decode.py:189-206): float64 softmax of scores*temperature. */
 int pqb_softmax_f64(const float* scores, int64_t n, double temperature, double* out,
                     pqb_stream_t stream);
+
+/* ------------------------------------------------- element-wise API ----
+ * The reference's array-level functions (polarquant.__init__:38-51), evaluated
+ * in the input's precision like numpy: dtype PQB_F32 (float32 arithmetic, the
+ * Python-float constants rounded to float32 first) or PQB_F64.  Operands are
+ * contiguous device arrays of n elements (the host broadcasts). */
+/* to_polar (polar_codec.py:200-209): r = hypot(x, y) (float32: glibc hypotf's
+ * fl32(sqrt(fl64(x^2 + y^2)))), t = mod(atan2(y, x) + pi, 2 pi) with a correctly
+ * rounded float32 atan2 (numpy's SIMD arctan2 may differ by a few ulp). */
+int pqb_to_polar(const void* x, const void* y, int dtype, int64_t n, void* radius_out, void* theta_out,
+                 pqb_stream_t stream);
+/* quantize_angle (polar_codec.py:212-221): uint8(int64(rint(t * 2^(m-1)/pi)) mod 2^m). */
+int pqb_quantize_angle(const void* theta, int dtype, int64_t n, int angle_bits, uint8_t* out, pqb_stream_t stream);
+/* angle_grid (polar_codec.py:224-233): pi * a / 2^(m-1) - pi, float64 [2^m]. */
+int pqb_angle_grid(int angle_bits, double* out, pqb_stream_t stream);
+/* quantize_radius / _quantize_radius_counted (polar_codec.py:254-278): rint(r / s)
+ * in r's precision (s already float32), 0 where s == 0, clipped to [0, 2^n - 1];
+ * clamped (nullable) += entries clamped from above. */
+int pqb_quantize_radius(const void* radius, int dtype, const float* scale, int64_t n, int radius_bits, uint8_t* out,
+                        unsigned long long* clamped, pqb_stream_t stream);
+/* qk_scores_direct (lut_decode.py:157-186): the dequantized keys of unit `unit`
+ * (bit-identical to pqb_dequantize) dotted with q [d] in fp32, then the residual
+ * keys; out[t] for t < min(tokens, seq_lens[unit]). */
+int pqb_scores_direct(const pqb_cache* cache, int64_t unit, const void* q, int q_dtype, int64_t tokens, float* out,
+                      pqb_stream_t stream);
+/* Scatter two contiguous reference streams of `tokens` tokens (PolarCodes /
+ * PQC1 payload, load_codes polar_codec.py:415-446, load_snapshot kv_cache.py:369-397)
+ * into unit `unit`'s pages: the inverse of pqb_export_streams.  Target pages
+ * must be zero past the imported bits (fresh), so later appends can OR codes in. */
+int pqb_import_streams(const pqb_store* store, int64_t unit, int d, int angle_bits, int radius_bits, int64_t tokens,
+                       const uint8_t* angle_stream, const uint8_t* radius_stream, pqb_stream_t stream);
 
 /* ------------------------------------------------------------ synthetic ----
  * Seeded on-device generator with gen_synthetic_keys' distribution

@@ -15,7 +15,16 @@ from .attention import (
     qk_scores_direct,
 )
 from .cache import PackedKVCache, PolarKVCache
-from .codec import compute_radius_scales, decode_keys, encode_keys
+from .codec import (
+    angle_grid,
+    compute_radius_scales,
+    decode_keys,
+    encode_keys,
+    quantize_angle,
+    quantize_radius,
+    to_polar,
+)
+from .container import CODES_MAGIC, load_codes, load_snapshot, save_codes, save_snapshot
 from .core import (
     AngleTable,
     BadMagicError,
@@ -40,6 +49,7 @@ from .synthetic import SyntheticConfig, gen_synthetic_keys, normal_device, synth
 __version__ = "0.1.0"
 
 __all__ = [
+    "CODES_MAGIC",
     "AngleTable",
     "BadMagicError",
     "BitReport",
@@ -57,6 +67,7 @@ __all__ = [
     "QueryLUT",
     "SyntheticConfig",
     "TruncatedFileError",
+    "angle_grid",
     "attention_weights",
     "build_angle_table",
     "build_query_lut",
@@ -65,11 +76,18 @@ __all__ = [
     "decode_keys",
     "encode_keys",
     "gen_synthetic_keys",
+    "load_codes",
+    "load_snapshot",
     "merge_pairs",
     "normal_device",
     "qk_scores",
     "qk_scores_direct",
+    "quantize_angle",
+    "quantize_radius",
+    "save_codes",
+    "save_snapshot",
     "split_pairs",
     "stream_bytes",
     "synthetic_keys_device",
+    "to_polar",
 ]

@@ -17,10 +17,12 @@ LIB_PATH = Path(__file__).resolve().parent / "libpqb200.so"
 PQB_OK, PQB_EINVAL, PQB_ESTATE, PQB_ECUDA, PQB_EUNSUPPORTED = 0, 1, 2, 3, 4
 PQB_FLAG_NONFINITE, PQB_FLAG_SCALE_OVERFLOW = 1, 2
 PQB_F32, PQB_BF16, PQB_F16 = 0, 1, 2
+PQB_F64 = 3  # element-wise reference API only
 PQB_VQ4 = 16  # pqb_store.value_dtype: 4-bit per-token value codes
 PQB_DECODE_FORCE_GENERIC, PQB_DECODE_NO_COMBINE, PQB_DECODE_DQ, PQB_DECODE_LUT = 1, 2, 4, 8
 PQB_DECODE_PROBE_MEM, PQB_DECODE_PROBE_COMPUTE = 64, 128
 PQB_DECODE_MERGE_KERNEL = 256
+PQB_DECODE_DQ_LINEAR = 512  # DQ kernel: linear shared-memory layout build (automatic fallback)
 
 c_i32, c_i64, c_u64, c_f32, c_f64, c_sz = (
     ctypes.c_int32,
@@ -155,6 +157,15 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     ),
     "pqb_quantize_values": (c_i32, [c_vp, c_i32, c_i64, c_i32, c_i32, c_vp, c_vp]),
     "pqb_softmax_f64": (c_i32, [c_vp, c_i64, c_f64, c_vp, c_vp]),
+    "pqb_to_polar": (c_i32, [c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
+    "pqb_quantize_angle": (c_i32, [c_vp, c_i32, c_i64, c_i32, c_vp, c_vp]),
+    "pqb_angle_grid": (c_i32, [c_i32, c_vp, c_vp]),
+    "pqb_quantize_radius": (c_i32, [c_vp, c_i32, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp]),
+    "pqb_scores_direct": (c_i32, [ctypes.POINTER(PqbCache), c_i64, c_vp, c_i32, c_i64, c_vp, c_vp]),
+    "pqb_import_streams": (
+        c_i32,
+        [ctypes.POINTER(PqbStore), c_i64, c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp],
+    ),
     "pqb_synthetic_keys": (
         c_i32,
         [c_u64, c_i64, c_i64, c_i32, c_i32, c_f32, c_f32, c_u64, c_f32, c_vp, c_i32, c_vp],

@@ -79,23 +79,22 @@ def qk_scores(query, cache: PackedKVCache, counter: OpCounter | None = None) -> 
 
 
 def qk_scores_direct(query, cache: PackedKVCache, counter: OpCounter | None = None) -> np.ndarray:
-    """Dequantize-then-dot path (lut_decode.py:157-186): GPU dequantization
-    (bit-identical x_hat/y_hat) followed by fp32 dot products."""
-    q = _query_row(query, cache).to(torch.float32)
+    """Dequantize-then-dot path (lut_decode.py:157-186): one kernel
+    (pqb_scores_direct) dequantizes every quantized key exactly as
+    decode_quantized (bit-identical x_hat/y_hat) and dots it with the query in
+    fp32, then the residual keys -- the reference's independent check of the
+    LUT path (agreement within 1e-4 of the peak, test_acceptance.py:64-92)."""
+    q = _query_row(query, cache).contiguous()
     dc = cache.device_cache
-    keys = dc.dequantize(0)
-    parts = [keys @ q] if keys.shape[0] else []
-    res = dc.residual_keys(0)
-    if res.shape[0]:
-        parts.append(res @ q)
+    T = cache.num_tokens
+    out = dc.scores_direct(q, 0, T)
     if counter is not None:
-        n = keys.shape[0] * cache.dim
+        n = cache.quantized_tokens * cache.dim
+        r = cache.residual_tokens * cache.dim
         counter.lookups += 3 * n // 2
-        counter.multiplies += 2 * n + res.numel()
-        counter.additions += n + res.numel()
-    if not parts:
-        return np.zeros(0, dtype=np.float32)
-    return torch.cat(parts).cpu().numpy().astype(np.float32)
+        counter.multiplies += 2 * n + r
+        counter.additions += n + r
+    return out.cpu().numpy()
 
 
 def attention_weights(scores, temperature: float) -> np.ndarray:

@@ -24,7 +24,9 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build" / "pqb200"
 LIB = PKG / "libpqb200.so"
-SOURCES = ["encode.cu", "encode_fast.cu", "decode.cu", "decode_dq.cu", "misc.cu", "abi.cu"]
+SOURCES = ["encode.cu", "encode_fast.cu", "decode.cu", "decode_dq.cu", "decode_dq_lin.cu", "misc.cu", "api.cu", "abi.cu"]
+# .cu files a source #includes (their text is part of its digest)
+INCLUDES = {"decode_dq_lin.cu": ["decode_dq.cu"]}
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = [
     "-O3",
@@ -48,7 +50,8 @@ def nvcc() -> str:
 def _digest(src: Path, extra: list[str]) -> str:
     h = hashlib.sha256()
     h.update(" ".join(extra).encode())
-    for p in sorted(list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "pqb200.h", src]):
+    deps = [CSRC / n for n in INCLUDES.get(src.name, [])]
+    for p in sorted(list(CSRC.glob("*.cuh")) + list(CSRC.glob("*.h")) + [ROOT / "include" / "pqb200.h", src] + deps):
         h.update(p.name.encode())
         h.update(p.read_bytes())
     return h.hexdigest()[:16]

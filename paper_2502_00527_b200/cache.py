@@ -124,6 +124,7 @@ class PolarKVCache:
         self._all_view: UnitView | None = None
         self.prefilled = False
         self.max_pages = 0
+        self._gen = 0  # storage generation: bumped whenever pool / page_table are replaced
         self._alloc(max(int(capacity), 1))
 
     # ------------------------------------------------------------ storage
@@ -142,6 +143,7 @@ class PolarKVCache:
             old = self.pool.view(U, self.max_pages, self.page_bytes)
             pool.view(U, max_pages, self.page_bytes)[:, : self.max_pages].copy_(old)
         self.pool, self.page_table, self.max_pages = pool, table.contiguous(), max_pages
+        self._gen += 1  # views built before this re-derive their descriptors (UnitView._sync)
         self._rebuild_struct()
 
     def _rebuild_struct(self) -> None:
@@ -251,24 +253,24 @@ class PolarKVCache:
         sub = self.sub_struct(u0, u1)
         sref = ctypes.byref(sub)
         n = u1 - u0
-        self.flags.zero_()
-        radius_scales_device(k, self.cfg, self.flags, self._scale_ws, out=self.scales16[u0:u1])
+        flags = new_flags(self.device)  # this call's faults only (self.flags keeps the unchecked ones)
+        radius_scales_device(k, self.cfg, flags, self._scale_ws, out=self.scales16[u0:u1])
         boundary = max(0, T - self.residual_len)
         if boundary:
             encode_device(k[:, :boundary], self.scales16[u0:u1], self.cfg, ctypes.byref(sub.store),
-                          clamp_counts=self.clamp_counts[u0:u1], flags=self.flags)
+                          clamp_counts=self.clamp_counts[u0:u1], flags=flags)
         if T > boundary:
             kr = k[:, boundary:]
             if kr.stride(-1) != 1:
                 kr = kr.contiguous()
             _lib.call("pqb_store_residual", sref, ptr(kr), dtype_code(kr), n, T - boundary,
-                      kr.stride(0), kr.stride(1), boundary, ptr(self.flags), stream_ptr(self.device))
+                      kr.stride(0), kr.stride(1), boundary, ptr(flags), stream_ptr(self.device))
         if v is not None and v.stride(-1) != 1:
             v = v.contiguous()
         _lib.call(
             "pqb_store_values_ex", ptr(v), dtype_code(v) if v is not None else 0, n, T, self.dim,
             v.stride(0) if v is not None else 0, v.stride(1) if v is not None else 0, ctypes.byref(sub.store),
-            None, 0, ptr(self.flags), stream_ptr(self.device),
+            None, 0, ptr(flags), stream_ptr(self.device),
         )
         self.seq_lens[u0:u1].fill_(T)
         self.quant_lens[u0:u1].fill_(boundary)
@@ -278,10 +280,77 @@ class PolarKVCache:
         self.prefilled = bool(self._filled.all())
         if check:
             try:
-                raise_on_flags(self.flags, "prefill")
+                raise_on_flags(flags, "prefill")
             except ValueError:
-                self.reset()
+                self._reset_units(u0, u1)  # units filled by earlier calls are kept
                 raise
+        else:
+            self.flags.bitwise_or_(flags)  # reported by check()
+
+    def import_unit(self, unit: int, codes: PolarCodes, scales: ChannelScales, residual_keys=None,
+                    clamp_events: int = 0, values=None) -> None:
+        """Load one unit from reference containers (load_codes / load_snapshot,
+        polar_codec.py:415-446, kv_cache.py:369-397): the two code streams are
+        scattered into the unit's pages (pqb_import_streams), the residual keys
+        (oldest first) fill the ring after them, values default to zeros.  The
+        unit then decodes and streams like a prefilled one."""
+        if not 0 <= unit < self.n_units:
+            raise ValueError(f"unit {unit} outside [0, {self.n_units})")
+        if self._filled[unit]:
+            raise RuntimeError("cache already prefilled")
+        cfg = codes.config()
+        if (cfg.angle_bits, cfg.radius_bits, cfg.layout) != (self.cfg.angle_bits, self.cfg.radius_bits,
+                                                             self.cfg.layout):
+            raise ValueError(f"codes config {cfg} does not match cache config {self.cfg}")
+        if codes.dim != self.dim or scales.num_channels != self.dim // 2:
+            raise ValueError(f"codes dim {codes.dim} / {scales.num_channels} scales != cache dim {self.dim}")
+        res = np.zeros((0, self.dim), np.float32) if residual_keys is None else np.asarray(residual_keys, np.float32)
+        if res.ndim != 2 or res.shape[1] != self.dim:
+            raise ValueError(f"residual keys must be (k, {self.dim}), got {res.shape}")
+        if res.shape[0] > self.residual_len:
+            raise ValueError(f"{res.shape[0]} residual keys exceed the window of {self.residual_len}")
+        Tq = codes.num_tokens
+        T = Tq + res.shape[0]
+        self.ensure_capacity(T)
+        sub = self.sub_struct(unit, unit + 1)
+        dev = self.device
+        if Tq:
+            a = torch.frombuffer(bytearray(codes.angle_stream), dtype=torch.uint8).to(dev)
+            r = torch.frombuffer(bytearray(codes.radius_stream), dtype=torch.uint8).to(dev)
+            _lib.call("pqb_import_streams", self.store_ref(), unit, self.dim, cfg.angle_bits, cfg.radius_bits, Tq,
+                      ptr(a), ptr(r), stream_ptr(dev))
+        self.scales16[unit] = torch.from_numpy(np.ascontiguousarray(scales.values, dtype=np.float16)).to(dev)
+        flags = new_flags(dev)
+        if res.shape[0]:
+            kr = torch.from_numpy(res).to(dev).unsqueeze(0)
+            _lib.call("pqb_store_residual", ctypes.byref(sub), ptr(kr), _lib.PQB_F32, 1, res.shape[0],
+                      kr.stride(0), kr.stride(1), Tq, ptr(flags), stream_ptr(dev))
+        v = None
+        if values is not None:
+            v = as_device_matrix(values, dev).reshape(1, T, self.dim).contiguous()
+        if T:
+            _lib.call("pqb_store_values_ex", ptr(v), dtype_code(v) if v is not None else 0, 1, T, self.dim,
+                      v.stride(0) if v is not None else 0, v.stride(1) if v is not None else 0,
+                      ctypes.byref(sub.store), None, 0, ptr(flags), stream_ptr(dev))
+        self.seq_lens[unit] = T
+        self.quant_lens[unit] = Tq
+        self.clamp_counts[unit] = int(clamp_events)
+        self.host_seq[unit] = T
+        self.host_quant[unit] = Tq
+        self._filled[unit] = True
+        self.prefilled = bool(self._filled.all())
+        try:
+            raise_on_flags(flags, "import")
+        except ValueError:
+            self._reset_units(unit, unit + 1)
+            raise
+
+    def snapshot_unit(self, unit: int = 0) -> CacheSnapshot:
+        """CacheSnapshot of one unit (kv_cache.py:261-268): packed streams
+        gathered from the pages, scales, residual keys oldest first."""
+        return CacheSnapshot(codes=self.export_codes(unit), scales=ChannelScales(self.scales16[unit].cpu().numpy()),
+                             residual_keys=self.residual_keys(unit).cpu().numpy(), residual_len=self.residual_len,
+                             clamp_events=int(self.clamp_counts[unit].item()))
 
     def append(self, keys, values=None, *, check: bool = False) -> None:
         """One streaming token per unit (kv_cache.py:179-189): keys/values [U, d]."""
@@ -297,14 +366,39 @@ class PolarKVCache:
         if values is not None:
             v = self._prepare(values, "value").reshape(self.n_units, self.dim).contiguous()
         self.ensure_capacity(int(self.host_seq.max()) + 2)
+        flags = new_flags(self.device) if check else self.flags  # unchecked faults stay for check()
         _lib.call("pqb_append", self.cache_ref(), self.n_units, ptr(k), dtype_code(k), ptr(v),
-                  dtype_code(v) if v is not None else 0, ptr(self.clamp_counts), ptr(self.flags),
+                  dtype_code(v) if v is not None else 0, ptr(self.clamp_counts), ptr(flags),
                   stream_ptr(self.device))
         flush = (self.host_seq - self.host_quant) >= self.residual_len
         self.host_quant = self.host_quant + flush.astype(np.int64)
         self.host_seq = self.host_seq + 1
-        if check:
-            raise_on_flags(self.flags, "append")
+        if check:  # the token is committed either way (the reference's append does not validate)
+            raise_on_flags(flags, "append")
+
+    def check(self) -> None:
+        """Raise ValueError if any unchecked prefill / append so far saw a
+        non-finite key or an fp16 scale overflow (synchronizes); clears the word."""
+        try:
+            raise_on_flags(self.flags, "cache")
+        finally:
+            self.flags.zero_()
+
+    def _reset_units(self, u0: int, u1: int) -> None:
+        """Return units [u0, u1) to the empty state: zero their pages (the
+        encoder ORs codes into fresh pages), lengths, scales and residual rows."""
+        ids = self.page_table[u0:u1].reshape(-1).long()
+        self.pool.view(-1, self.page_bytes).index_fill_(0, ids, 0)
+        self.seq_lens[u0:u1] = 0
+        self.quant_lens[u0:u1] = 0
+        self.clamp_counts[u0:u1] = 0
+        self.scales16[u0:u1] = 0
+        if self.residual is not None:
+            self.residual[u0:u1] = 0
+        self.host_seq[u0:u1] = 0
+        self.host_quant[u0:u1] = 0
+        self._filled[u0:u1] = False
+        self.prefilled = False
 
     def reset(self) -> None:
         self.pool.zero_()
@@ -322,7 +416,7 @@ class PolarKVCache:
     # ------------------------------------------------------------ decode
 
     def _all(self) -> "UnitView":
-        if self._all_view is None or self._all_view.struct.store.pool != ptr(self.pool):
+        if self._all_view is None:
             self._all_view = UnitView(self, 0, self.n_units)
         return self._all_view
 
@@ -384,6 +478,16 @@ class PolarKVCache:
             _lib.call("pqb_dequantize", self.cache_ref(), unit, Tq, ptr(out), stream_ptr(self.device))
         return out
 
+    def scores_direct(self, q: torch.Tensor, unit: int = 0, tokens: int | None = None) -> torch.Tensor:
+        """qk_scores_direct of one unit (lut_decode.py:157-186): dequantized keys
+        dotted with q [d] in fp32, then the residual keys; fp32 [T]."""
+        T = int(self.host_seq[unit]) if tokens is None else int(tokens)
+        out = torch.empty(max(T, 0), dtype=torch.float32, device=self.device)
+        if T:
+            _lib.call("pqb_scores_direct", self.cache_ref(), unit, ptr(q), dtype_code(q), T, ptr(out),
+                      stream_ptr(self.device))
+        return out
+
     def radius_table(self) -> torch.Tensor:
         half = self.dim // 2
         L = self.cfg.radius_levels
@@ -396,16 +500,25 @@ class PolarKVCache:
 class UnitView:
     """Decode entry for units [u0, u1) of a PolarKVCache (e.g. one layer).
 
-    Holds its own C descriptor so repeated calls (or CUDA-graph capture) need
-    no per-call host work beyond argument marshalling."""
+    Holds its own C descriptor so repeated calls need no per-call host work
+    beyond argument marshalling.  The descriptor is re-derived whenever the
+    cache has replaced its pool / page table (growth on append), so a view
+    never reads freed storage.  A CUDA graph captured before such a growth
+    still holds the old pointers and must be re-captured."""
 
     def __init__(self, cache: PolarKVCache, u0: int, u1: int) -> None:
         self.cache = cache
         self.u0, self.u1 = u0, u1
         self.n_units = u1 - u0
-        self.struct = cache.sub_struct(u0, u1)
-        self.ref = ctypes.byref(self.struct)
         self._ws: torch.Tensor | None = None
+        self._gen = -1
+        self._sync()
+
+    def _sync(self) -> None:
+        if self._gen != self.cache._gen:
+            self.struct = self.cache.sub_struct(self.u0, self.u1)
+            self.ref = ctypes.byref(self.struct)
+            self._gen = self.cache._gen
 
     def workspace(self, group: int, max_tokens: int) -> torch.Tensor:
         """Per-view decode workspace.  Zero-filled once: its leading counter
@@ -421,6 +534,7 @@ class UnitView:
 
     def _check_q(self, q) -> torch.Tensor:
         c = self.cache
+        self._sync()
         if not c._filled[self.u0 : self.u1].all():
             raise RuntimeError("cache is empty; prefill first")
         q = as_device_matrix(q, c.device)
@@ -558,6 +672,26 @@ class PackedKVCache:
             raise RuntimeError("cache is empty; prefill first")
         return self._dev
 
+    @classmethod
+    def from_snapshot(cls, snap: CacheSnapshot, device=None) -> "PackedKVCache":
+        """A prefilled cache restored from a snapshot (load_snapshot,
+        kv_cache.py:363-397): codes, scales, residual window and clamp count;
+        values are zeros; further appends continue the stream."""
+        cache = cls(snap.codes.config(), snap.residual_len, device=device)
+        dev = require_cuda(device)
+        d = snap.codes.dim
+        T = snap.codes.num_tokens + np.asarray(snap.residual_keys).shape[0]
+        cache._dim = d
+        cache._dev = PolarKVCache(cache.cfg, 1, d, snap.residual_len, capacity=max(T + 64, 128), page_tokens=64,
+                                  value_dtype=torch.float32, device=dev)
+        try:
+            cache._dev.import_unit(0, snap.codes, snap.scales, snap.residual_keys, snap.clamp_events)
+        except Exception:
+            cache._dev = None
+            cache._dim = None
+            raise
+        return cache
+
     # -- writes ----------------------------------------------------------
 
     def _value_rows(self, values, count: int) -> torch.Tensor | None:
@@ -571,6 +705,8 @@ class PackedKVCache:
         if self.quantize_values:
             if not 1 <= self.value_bits <= 8:
                 raise ValueError(f"bits must be in [1, 8], got {self.value_bits}")
+            if not bool(torch.isfinite(v).all()):  # quantize_uniform, baseline_quant.py:88-89 (before any write)
+                raise ValueError("values contain non-finite entries")
             out = torch.empty((count, self._dim), dtype=torch.float32, device=dev)
             v = v.contiguous()
             _lib.call("pqb_quantize_values", ptr(v), dtype_code(v), count, self._dim, self.value_bits, ptr(out),
@@ -616,7 +752,9 @@ class PackedKVCache:
                                  else value.reshape(1, -1), 1)
         elif self.quantize_values:
             v = self._value_rows(np.zeros((1, self._dim), dtype=np.float32), 1)
-        self._dev.append(row.unsqueeze(0), v, check=True)
+        # the reference's append does not validate keys (kv_cache.py:179-189): a
+        # non-finite key is committed like any other, and later appends still work
+        self._dev.append(row.unsqueeze(0), v, check=False)
         self._consolidated = None
 
     # -- reads -----------------------------------------------------------

@@ -26,7 +26,7 @@ from ._device import (
     require_cuda,
     stream_ptr,
 )
-from .core import ChannelScales, KeyTensor, PolarCodes, QuantConfig, merge_pairs, stream_bytes
+from .core import ChannelScales, KeyTensor, PolarCodes, QuantConfig, _check_bits, merge_pairs, stream_bytes
 
 
 def radius_scales_device(keys: torch.Tensor, cfg: QuantConfig, flags: torch.Tensor | None = None,
@@ -197,3 +197,99 @@ __all__ = [
     "pack_code_arrays",
     "merge_pairs",
 ]
+
+
+# ------------------------------------------------------------------ element-wise
+# The reference's array-level functions (polar_codec.py:200-278), on the GPU.
+# numpy computes them in the operands' precision (NEP 50: Python floats are weak
+# and take the array's dtype), so float32 arrays run the float32 kernels and
+# float64 arrays / Python scalars / integers the float64 ones.  Inputs are
+# broadcast on the host like numpy; 0-d inputs return numpy scalars.
+
+
+def _precision(*xs) -> np.dtype:
+    dt = np.result_type(*(x if isinstance(x, (int, float, np.ndarray, np.generic)) else np.asarray(x) for x in xs))
+    if dt == np.float32 or dt == np.float16:  # float16: computed in float32 (numpy would round each step to fp16)
+        return np.dtype(np.float32)
+    return np.dtype(np.float64)
+
+
+def _to_device(a: np.ndarray, dev: torch.device) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def _scalar_or_array(out: np.ndarray, ndim: int):
+    return out[()] if ndim == 0 else out
+
+
+def to_polar(x, y) -> tuple[np.ndarray, np.ndarray]:
+    """(radius, angle) of Cartesian components (polar_codec.py:200-209):
+    radius = hypot(x, y), angle = mod(atan2(y, x) + pi, 2 pi) in [0, 2 pi);
+    the origin maps to angle pi.  float32: hypotf's exact rounding and a
+    correctly rounded atan2 (numpy's SIMD arctan2 may differ by a few ulp)."""
+    dev = require_cuda()
+    dt = _precision(x, y)
+    xb, yb = np.broadcast_arrays(np.asarray(x, dtype=dt), np.asarray(y, dtype=dt))
+    n = xb.size
+    xd, yd = _to_device(xb.reshape(-1), dev), _to_device(yb.reshape(-1), dev)
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    r = torch.empty(n, dtype=tdt, device=dev)
+    t = torch.empty(n, dtype=tdt, device=dev)
+    if n:
+        _lib.call("pqb_to_polar", ptr(xd), ptr(yd), _lib.PQB_F32 if dt == np.float32 else _lib.PQB_F64, n, ptr(r),
+                  ptr(t), stream_ptr(dev))
+    shape = xb.shape
+    return (_scalar_or_array(r.cpu().numpy().reshape(shape), len(shape)),
+            _scalar_or_array(t.cpu().numpy().reshape(shape), len(shape)))
+
+
+def quantize_angle(theta, angle_bits: int) -> np.ndarray:
+    """Nearest point of the circular 2^m grid, half-even, wrapping 2 pi to 0
+    (polar_codec.py:212-221)."""
+    _check_bits(angle_bits, "angle_bits")
+    dev = require_cuda()
+    dt = _precision(theta)
+    th = np.asarray(theta, dtype=dt)
+    n = th.size
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    if n:
+        _lib.call("pqb_quantize_angle", ptr(_to_device(th.reshape(-1), dev)),
+                  _lib.PQB_F32 if dt == np.float32 else _lib.PQB_F64, n, angle_bits, ptr(out), stream_ptr(dev))
+    return _scalar_or_array(out.cpu().numpy().reshape(th.shape), th.ndim)
+
+
+def angle_grid(angle_bits: int) -> np.ndarray:
+    """Decoded angle of every code, float64, in [-pi, pi) (polar_codec.py:224-233)."""
+    _check_bits(angle_bits, "angle_bits")
+    dev = require_cuda()
+    out = torch.empty(1 << angle_bits, dtype=torch.float64, device=dev)
+    _lib.call("pqb_angle_grid", angle_bits, ptr(out), stream_ptr(dev))
+    return out.cpu().numpy()
+
+
+def quantize_radius_counted(radius, scale, radius_bits: int) -> tuple[np.ndarray, int]:
+    """_quantize_radius_counted (polar_codec.py:267-278): codes plus the number
+    of entries clamped from above."""
+    _check_bits(radius_bits, "radius_bits")
+    dev = require_cuda()
+    r = np.asarray(radius)
+    s32 = np.asarray(scale).astype(np.float32)
+    dt = _precision(r, s32)
+    rb, sb = np.broadcast_arrays(r.astype(dt, copy=False), s32)
+    n = rb.size
+    out = torch.empty(n, dtype=torch.uint8, device=dev)
+    clamped = torch.zeros(1, dtype=torch.int64, device=dev)
+    if n:
+        _lib.call("pqb_quantize_radius", ptr(_to_device(rb.reshape(-1), dev)),
+                  _lib.PQB_F32 if dt == np.float32 else _lib.PQB_F64, ptr(_to_device(sb.reshape(-1), dev)), n,
+                  radius_bits, ptr(out), ptr(clamped), stream_ptr(dev))
+    return _scalar_or_array(out.cpu().numpy().reshape(rb.shape), rb.ndim), int(clamped.item())
+
+
+def quantize_radius(radius, scale, radius_bits: int) -> np.ndarray:
+    """Round radii to code * scale points, clamping to the code range; zero
+    scales force code 0; broadcasting applies (polar_codec.py:254-264)."""
+    return quantize_radius_counted(radius, scale, radius_bits)[0]
+
+
+__all__ += ["to_polar", "quantize_angle", "angle_grid", "quantize_radius"]

@@ -353,6 +353,62 @@ int pqb_softmax_f64(const float* scores, int64_t n, double temperature, double* 
   return cuda_status("pqb_softmax_f64");
 }
 
+int pqb_to_polar(const void* x, const void* y, int dtype, int64_t n, void* radius_out, void* theta_out,
+                 pqb_stream_t stream) {
+  PQB_CHECK(dtype == PQB_F32 || dtype == PQB_F64, PQB_EINVAL, "to_polar: dtype must be PQB_F32 or PQB_F64");
+  PQB_CHECK(n >= 0 && (n == 0 || (x && y && radius_out && theta_out)), PQB_EINVAL, "bad arguments");
+  launch_to_polar(x, y, dtype, n, radius_out, theta_out, reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status("pqb_to_polar");
+}
+
+int pqb_quantize_angle(const void* theta, int dtype, int64_t n, int angle_bits, uint8_t* out, pqb_stream_t stream) {
+  PQB_CHECK(angle_bits >= 1 && angle_bits <= 8, PQB_EINVAL, "angle_bits must be in [1, 8], got %d", angle_bits);
+  PQB_CHECK(dtype == PQB_F32 || dtype == PQB_F64, PQB_EINVAL, "quantize_angle: dtype must be PQB_F32 or PQB_F64");
+  PQB_CHECK(n >= 0 && (n == 0 || (theta && out)), PQB_EINVAL, "bad arguments");
+  launch_quantize_angle(theta, dtype, n, angle_bits, out, reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status("pqb_quantize_angle");
+}
+
+int pqb_angle_grid(int angle_bits, double* out, pqb_stream_t stream) {
+  PQB_CHECK(angle_bits >= 1 && angle_bits <= 8, PQB_EINVAL, "angle_bits must be in [1, 8], got %d", angle_bits);
+  PQB_CHECK(out, PQB_EINVAL, "null output");
+  launch_angle_grid(angle_bits, out, reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status("pqb_angle_grid");
+}
+
+int pqb_quantize_radius(const void* radius, int dtype, const float* scale, int64_t n, int radius_bits, uint8_t* out,
+                        unsigned long long* clamped, pqb_stream_t stream) {
+  PQB_CHECK(radius_bits >= 1 && radius_bits <= 8, PQB_EINVAL, "radius_bits must be in [1, 8], got %d", radius_bits);
+  PQB_CHECK(dtype == PQB_F32 || dtype == PQB_F64, PQB_EINVAL, "quantize_radius: dtype must be PQB_F32 or PQB_F64");
+  PQB_CHECK(n >= 0 && (n == 0 || (radius && scale && out)), PQB_EINVAL, "bad arguments");
+  launch_quantize_radius(radius, dtype, scale, n, radius_bits, out, clamped, reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status("pqb_quantize_radius");
+}
+
+int pqb_scores_direct(const pqb_cache* cache, int64_t unit, const void* q, int q_dtype, int64_t tokens, float* out,
+                      pqb_stream_t stream) {
+  PQB_CHECK(cache && cache->scales && cache->seq_lens && cache->quant_lens, PQB_ESTATE,
+            "cache is empty; prefill first");
+  PQB_CHECK(q && dtype_ok(q_dtype) && unit >= 0 && tokens >= 0 && (tokens == 0 || out), PQB_EINVAL,
+            "bad arguments");
+  const int rc = check_store(&cache->store, cache->d, cache->angle_bits, cache->radius_bits, false);
+  if (rc) return rc;
+  launch_scores_direct(*cache, unit, q, q_dtype, tokens, out, reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status("pqb_scores_direct");
+}
+
+int pqb_import_streams(const pqb_store* store, int64_t unit, int d, int angle_bits, int radius_bits, int64_t tokens,
+                       const uint8_t* angle_stream, const uint8_t* radius_stream, pqb_stream_t stream) {
+  const int rc = check_store(store, d, angle_bits, radius_bits, false);
+  if (rc) return rc;
+  PQB_CHECK(tokens >= 0 && tokens <= static_cast<int64_t>(store->max_pages) * store->page_tokens, PQB_EINVAL,
+            "tokens out of range");
+  PQB_CHECK(unit >= 0 && (tokens == 0 || (angle_stream && radius_stream)), PQB_EINVAL, "bad arguments");
+  launch_import(*store, unit, d, angle_bits, radius_bits, tokens, angle_stream, radius_stream,
+                reinterpret_cast<cudaStream_t>(stream));
+  return cuda_status("pqb_import_streams");
+}
+
 int pqb_synthetic_keys(uint64_t seed, int64_t n_units, int64_t tokens, int d, int layout, float radius_log_mean,
                        float radius_log_std, uint64_t outlier_mask, float outlier_boost, void* out, int out_dtype,
                        pqb_stream_t stream) {

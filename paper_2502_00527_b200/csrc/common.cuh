@@ -9,11 +9,45 @@
 #include <cuda_fp16.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/pqb200.h"
 
 #define PQB_DEV __device__ __forceinline__
 
 namespace pqb {
+
+// ------------------------------------------------------- host: per device
+// One-time setup per device ordinal (kernel attributes, SM counts), safe for
+// concurrent callers and for one process driving several GPUs: a bit per
+// device, set after the setup succeeded (a race at worst repeats an
+// idempotent cudaFuncSetAttribute).
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+template <typename F>
+inline int once_per_device(std::atomic<uint64_t>& done, F&& setup) {
+  const uint64_t bit = 1ull << (current_device() & 63);
+  if (done.load(std::memory_order_acquire) & bit) return PQB_OK;
+  const int rc = setup();
+  if (rc == PQB_OK) done.fetch_or(bit, std::memory_order_acq_rel);
+  return rc;
+}
+
+// SM count of the current device (148 on B200), cached per device.
+inline int device_sms() {
+  static std::atomic<int> cache[64];
+  const int dev = current_device();
+  int n = cache[dev & 63].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev & 63].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
 
 constexpr int kWarp = 32;
 

@@ -557,15 +557,7 @@ __global__ void combine_kernel(const float* __restrict__ part_ml, const float* _
 
 // ------------------------------------------------------------------ host side
 
-static int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-  }
-  return sms;
-}
+static int num_sms() { return device_sms(); }
 
 constexpr int kMaxCtas = 256;  // bound used to size the partial-slot workspace
 
@@ -652,15 +644,16 @@ static int fast_setup(const DecodeArgs& a, EpiArgs& ep, WorkSplit& ws, int& grid
 template <int G, int M, int N, bool EXACT>
 static int launch_fast(const DecodeArgs& a, cudaStream_t s) {
   using Cfg = FastCfg<G, M, N, EXACT>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_done{0};
+  const int arc = once_per_device(attr_done, [] {
     if (cudaFuncSetAttribute(decode_fast_kernel<G, M, N, EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg::kSmem) != cudaSuccess) {
       set_error("cudaFuncSetAttribute(smem=%d) failed", Cfg::kSmem);
       return PQB_ECUDA;
     }
-    attr_set = true;
-  }
+    return PQB_OK;
+  });
+  if (arc != PQB_OK) return arc;
   EpiArgs ep;
   WorkSplit ws;
   int grid = 0;
@@ -715,7 +708,8 @@ static int launch_dq_path(const DecodeArgs& a, cudaStream_t s, bool& handled) {
   const bool sep = ep.merge && a.out != nullptr && a.peer == nullptr &&
                    separate_merge(a.flags, a.group, a.max_tokens, ws);
   if (sep) ep.merge = false;
-  const int rc2 = launch_decode_dq(a, ep, ws, grid, s, handled);
+  int rc2 = (a.flags & PQB_DECODE_DQ_LINEAR) ? kDqLayoutUnavailable : dq_prmt::launch_decode_dq(a, ep, ws, grid, s, handled);
+  if (rc2 == kDqLayoutUnavailable) rc2 = dq_lin::launch_decode_dq(a, ep, ws, grid, s, handled);
   if (rc2 != PQB_OK || !handled || !sep) return rc2;
   return launch_merge_split(ep, ws, a.n_units, s);
 }
@@ -791,10 +785,19 @@ int launch_decode(const DecodeArgs& a, cudaStream_t s) {
   }
   const size_t shm = sizeof(float) * (a.group * c.d + 512 + c.d / 2 + kNW * kTile * a.group +
                                       kNW * a.group * (2 + c.d));
-  static size_t attr = 0;
-  if (shm > 48 * 1024 && shm > attr) {
-    cudaFuncSetAttribute(decode_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(shm));
-    attr = shm;
+  static std::atomic<size_t> attr[64];  // largest opt-in set so far, per device
+  if (shm > 48 * 1024) {
+    std::atomic<size_t>& cur = attr[current_device() & 63];
+    if (shm > cur.load(std::memory_order_acquire)) {
+      if (cudaFuncSetAttribute(decode_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(shm)) != cudaSuccess) {
+        set_error("cudaFuncSetAttribute(smem=%zu) failed", shm);
+        return PQB_ECUDA;
+      }
+      size_t seen = cur.load(std::memory_order_acquire);
+      while (seen < shm && !cur.compare_exchange_weak(seen, shm, std::memory_order_acq_rel)) {
+      }
+    }
   }
   dim3 grid(splits, static_cast<unsigned>(a.n_units));
   decode_generic_kernel<<<grid, kNW * 32, shm, s>>>(c, a.group, a.q, a.q_dtype, a.sm_scale * kLog2e, a.scores,

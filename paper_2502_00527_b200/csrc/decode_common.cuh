@@ -294,8 +294,18 @@ PQB_DEV void finish_segment(const EpiArgs& ep, const WorkSplit& ws, int64_t unit
 
 struct DecodeArgs;
 // decode_dq.cu: dequantize + tensor-core scoring variant of the fused kernel
-// (G in {4, 8}, fused output only).  handled = false when (m, n) has no instance.
+// (G in {4, 8}).  handled = false when (m, n) has no instance.  Two builds:
+// dq_prmt (product table at a fixed shared-window address, the default) returns
+// kDqLayoutUnavailable when this device's shared window is laid out so the
+// table cannot sit there; dq_lin (decode_dq_lin.cu, linear layout) always runs.
+constexpr int kDqLayoutUnavailable = -1;
+namespace dq_prmt {
 int launch_decode_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s,
                      bool& handled);
+}
+namespace dq_lin {
+int launch_decode_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s,
+                     bool& handled);
+}
 
 }  // namespace pqb

@@ -47,7 +47,21 @@
 
 #include <algorithm>
 
+// the product-table layout (see kPtTabAbs below); before DqCfg, which sizes by it.
+// The library carries both builds: this file (PRMT table, namespace dq_prmt)
+// and decode_dq_lin.cu (the same source with the linear layout, dq_lin), the
+// runtime fallback when the shared window is laid out other than measured.
+#ifndef PQB_DQ_PRMT_TAB
+#define PQB_DQ_PRMT_TAB 1
+#endif
+#if PQB_DQ_PRMT_TAB
+#define PQB_DQ_NS dq_prmt
+#else
+#define PQB_DQ_NS dq_lin
+#endif
+
 namespace pqb {
+namespace PQB_DQ_NS {
 
 // Warp specialisation: a fourth warpgroup of producers (warp kNW + j fills the
 // rings of compute warps j and j + 4, which share its SM sub-partition) takes
@@ -56,10 +70,6 @@ namespace pqb {
 // PQB_DQ_WS=0 builds the previous layout (lane 0 of each compute warp issues).
 #ifndef PQB_DQ_WS
 #define PQB_DQ_WS 1
-#endif
-// the product-table layout (see kPtTabAbs below); before DqCfg, which sizes by it
-#ifndef PQB_DQ_PRMT_TAB
-#define PQB_DQ_PRMT_TAB 1
 #endif
 #ifndef PQB_DQ_CONS_REGS
 #define PQB_DQ_CONS_REGS 232
@@ -422,7 +432,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           c1.init(t_lo + w1, tpp);
           auto issue = [&](int w, uint32_t it, const TileCursor& cu) {
             const uint32_t s = it % kStages;
-            mbar_wait(&s_empty[w][s], ((it / kStages) & 1) ^ 1);
+            // the ring starts empty: the first kStages fills need no release
+            if (it >= kStages) mbar_wait(&s_empty[w][s], ((it / kStages) & 1) ^ 1);
             fence_proxy_async_smem();
             issue_tile_dq<M, N, VQ, kScores>(stage_ptr(w * kStages + s), c.store,
                                     page_base_c(c.store, unit, PROBE == 2 ? 0 : cu.pg), PROBE == 2 ? 0 : cu.tin,
@@ -835,14 +846,13 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 template <int G, int M, int N, int PROBE = 0, int VQ = 0>
 static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s) {
   using Cfg = DqCfg<G, M, N, VQ>;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static std::atomic<uint64_t> attr_done{0};
+  const int arc = once_per_device(attr_done, [] {
 #if PQB_DQ_PRMT_TAB
     {  // the table must land at kPtTabAbs with the stages around it (as the kernel assumes)
       cudaFuncAttributes fa;
-      int dev = 0, reserved = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+      int reserved = 0;
+      cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, current_device());
       if (cudaFuncGetAttributes(&fa, decode_dq_kernel<G, M, N, PROBE, VQ>) != cudaSuccess) {
         set_error("cudaFuncGetAttributes failed");
         return PQB_ECUDA;
@@ -855,11 +865,8 @@ static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws
       const int n_before = tab_off / Cfg::kStageBytes;
       if (tab_off < 0 || n_before * Cfg::kStageBytes < kNW * G * 132 * 4 ||
           tab_off + 65536 + (kNW * kStages - n_before) * Cfg::kStageBytes > Cfg::kSmem ||
-          stat + Cfg::kSmem > 232448) {
-        set_error("decode_dq: shared-window layout (reserved %d, static %d) leaves no room for the table at 0x%x",
-                  reserved, stat, kPtTabAbs);
-        return PQB_ECUDA;
-      }
+          stat + Cfg::kSmem > 232448)
+        return kDqLayoutUnavailable;  // the caller falls back to the linear-layout build
     }
 #endif
     if (cudaFuncSetAttribute(decode_dq_kernel<G, M, N, PROBE, VQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -867,8 +874,9 @@ static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws
       set_error("cudaFuncSetAttribute(smem=%d) failed", Cfg::kSmem);
       return PQB_ECUDA;
     }
-    attr_set = true;
-  }
+    return PQB_OK;
+  });
+  if (arc != PQB_OK) return arc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kDqThreads);
@@ -935,4 +943,5 @@ int launch_decode_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws
   return PQB_OK;
 }
 
+}  // namespace PQB_DQ_NS
 }  // namespace pqb

@@ -872,12 +872,11 @@ static void launch_rmax_v8(const RadiusScalesArgs& a, int64_t chunk, dim3 grid, 
 
 template <int DT, int LAYOUT>
 static void launch_rmax_tma(const RadiusScalesArgs& a, int64_t chunk, dim3 grid, size_t shm, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(radius_max_tma_kernel<DT, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(shm));
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  once_per_device(attr_done, [shm] {
+    return cudaFuncSetAttribute(radius_max_tma_kernel<DT, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(shm)) == cudaSuccess ? PQB_OK : PQB_ECUDA;
+  });
   radius_max_tma_kernel<DT, LAYOUT><<<grid, 256, shm, s>>>(a.keys, a.tokens, a.d / 2, a.unit_stride, chunk,
                                                            a.maxsq_ws);
 }

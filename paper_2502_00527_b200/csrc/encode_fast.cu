@@ -526,25 +526,17 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
 }
 
 int ef_num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+  return device_sms();
 }
 
 template <int DT, int LAYOUT, int M, int N>
 void launch_ef(const EfArgs& p, cudaStream_t s) {
   using Cfg = EfCfg<DT>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(encode_fast_kernel<DT, LAYOUT, M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg::kSmem);
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  once_per_device(attr_done, [] {
+    return cudaFuncSetAttribute(encode_fast_kernel<DT, LAYOUT, M, N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                Cfg::kSmem) == cudaSuccess ? PQB_OK : PQB_ECUDA;
+  });
   const int64_t grid = std::min<int64_t>((p.items + kEfWarps - 1) / kEfWarps, ef_num_sms());
   encode_fast_kernel<DT, LAYOUT, M, N><<<static_cast<unsigned>(grid), kEfWarps * 32, Cfg::kSmem, s>>>(p);
 }

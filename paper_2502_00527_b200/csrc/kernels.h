@@ -93,6 +93,17 @@ int launch_synthetic_keys(uint64_t seed, int64_t n_units, int64_t T, int d, int 
                           uint64_t mask, float boost, void* out, int dtype, cudaStream_t s);
 int launch_synthetic_normal(uint64_t seed, int64_t count, void* out, int dtype, cudaStream_t s);
 
+// api.cu: element-wise reference API, PQC1 import, qk_scores_direct
+int launch_to_polar(const void* x, const void* y, int dtype, int64_t n, void* r, void* t, cudaStream_t s);
+int launch_quantize_angle(const void* theta, int dtype, int64_t n, int m, uint8_t* out, cudaStream_t s);
+int launch_angle_grid(int m, double* out, cudaStream_t s);
+int launch_quantize_radius(const void* radius, int dtype, const float* scale, int64_t n, int bits, uint8_t* out,
+                           unsigned long long* clamped, cudaStream_t s);
+int launch_import(const pqb_store& st, int64_t unit, int d, int m, int n, int64_t T, const uint8_t* a,
+                  const uint8_t* r, cudaStream_t s);
+int launch_scores_direct(const pqb_cache& c, int64_t unit, const void* q, int q_dtype, int64_t tokens, float* out,
+                         cudaStream_t s);
+
 void set_error(const char* fmt, ...);
 
 }  // namespace pqb

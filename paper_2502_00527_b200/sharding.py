@@ -143,12 +143,21 @@ def plan_for(shape: DecodeShape, world: int, rank: int, head: bool) -> ShardPlan
 
 
 class PeerGather:
-    """Gathered per-layer outputs [L, B, Hq, d] shared by the ranks of one node.
+    """Gathered per-layer outputs [2, L, B, Hq, d] shared by the ranks of one node.
 
     Every rank allocates its own buffer and a flag array [L, world] (uint32,
     zero), then all ranks exchange CUDA IPC handles (torch's CUDA tensor
     reduction, sent through ``dist.all_gather_object``) and open each other's
-    buffers, so the decode epilogue can store into all of them directly."""
+    buffers, so the decode epilogue can store into all of them directly.
+
+    Steps alternate between two buffers (``parity``).  Step k's decode writes
+    buffer k % 2 of every peer once the writing rank has seen step k - 1
+    complete on all ranks, i.e. once every rank's stream has run its step k - 1
+    decodes -- and with them anything it enqueued before them that reads step
+    k - 2's outputs (buffer k % 2).  Contract: a rank consumes step k's
+    outputs (``out[k % 2]``) on its decode stream before it enqueues step
+    k + 2's decode.  With one buffer a fast rank's step k + 1 stores could
+    overwrite rows a slow rank had not yet read."""
 
     def __init__(self, plan: ShardPlan, device, group=None, dtype=torch.bfloat16) -> None:
         import torch.distributed as dist
@@ -158,9 +167,10 @@ class PeerGather:
         if plan.world > 8:
             raise ValueError("peer gather supports up to 8 ranks")
         self.plan, self.dtype = plan, dtype
-        self.out = torch.zeros((S.layers, S.batch, S.q_heads, S.head_dim), dtype=dtype, device=device)
+        self.out = torch.zeros((2, S.layers, S.batch, S.q_heads, S.head_dim), dtype=dtype, device=device)
         self.flags = torch.zeros((S.layers, plan.world), dtype=torch.int32, device=device)  # counts, peers add
         self.expect = torch.zeros(S.layers, dtype=torch.int32, device=device)  # this rank's per-layer count
+        self.parity = 0
         torch.cuda.synchronize(device)
         mine = (reduce_tensor(self.out), reduce_tensor(self.flags))
         handles = [None] * plan.world
@@ -173,19 +183,27 @@ class PeerGather:
             else:
                 self.peer_out.append(ho[0](*ho[1]))
                 self.peer_flags.append(hf[0](*hf[1]))
-        self._desc = [self._descriptor(layer) for layer in range(S.layers)]
+        self._desc = [[self._descriptor(p, layer) for layer in range(S.layers)] for p in range(2)]
 
-    def descriptor(self, layer: int):
-        return self._desc[layer]
+    def next_step(self) -> int:
+        """Start a step: flip to the other buffer; returns its parity."""
+        self.parity ^= 1
+        return self.parity
 
-    def _descriptor(self, layer: int):
+    def descriptor(self, layer: int, parity: int | None = None):
+        return self._desc[self.parity if parity is None else parity][layer]
+
+    def gathered(self, layer: int, parity: int | None = None) -> torch.Tensor:
+        return self.out[self.parity if parity is None else parity, layer]
+
+    def _descriptor(self, parity: int, layer: int):
         from . import _lib
         from ._device import dtype_code
 
         p, S = self.plan, self.plan.shape
         d = _lib.PqbPeerOut()
         for k in range(p.world):
-            d.out[k] = self.peer_out[k][layer].data_ptr()
+            d.out[k] = self.peer_out[k][parity, layer].data_ptr()
             d.flags[k] = self.peer_flags[k][layer].data_ptr()
         d.n_peers, d.rank = p.world, p.rank
         d.batch0, d.head0, d.kv_local, d.q_heads = p.b0, p.h0, p.kv_heads, S.q_heads
@@ -220,14 +238,24 @@ class HeadShardedDecoder:
         self.peers = PeerGather(plan, cache.device, group, out_dtype) if gather == "p2p" else None
 
     def layer(self, layer: int, q_layer: torch.Tensor, wait: bool = True) -> torch.Tensor:
+        """One layer of the current step (p2p: into buffer ``peers.parity``;
+        call ``begin_step()`` before a step's first layer).  The p2p result is
+        a view of the shared buffer, valid until the step after next."""
         q_loc = local_queries(q_layer, self.plan)
         if self.peers is not None:
             self.views[layer].decode_peer(q_loc, self.peers.descriptor(layer))
             if wait:
                 self.peers.wait(layer)
-            return self.peers.out[layer]
+            return self.peers.gathered(layer)
         local = self.views[layer].decode(q_loc, out_dtype=self.out_dtype)
         return gather_head_outputs(local, self.plan, self.group)
 
+    def begin_step(self) -> None:
+        if self.peers is not None:
+            self.peers.next_step()
+
     def step(self, q: torch.Tensor) -> torch.Tensor:
+        """All layers for q [L, B, Hq, d]; returns a fresh [L, B, Hq, d]
+        (copied on the decode stream, as the double-buffer contract needs)."""
+        self.begin_step()
         return torch.stack([self.layer(layer, q[layer]) for layer in range(self.plan.shape.layers)])

@@ -43,8 +43,9 @@ def _worker(rank, world, port, G, result_dir):
         T = 700
         rng = np.random.default_rng(0)
         vals = rng.standard_normal((shape.layers, shape.batch, shape.kv_heads, T, 128)).astype(np.float32)
-        q = torch.from_numpy(rng.standard_normal((shape.layers, shape.batch, shape.q_heads, 128)).astype(np.float32))
-        q = q.to(torch.bfloat16).cuda()
+        qs = torch.from_numpy(rng.standard_normal((4, shape.layers, shape.batch, shape.q_heads, 128)).astype(np.float32))
+        qs = qs.to(torch.bfloat16).cuda()
+        q = qs[0]
         cfg = pq.QuantConfig(4, 4)
         # this rank's shard, units in plan.unit_index order
         cache = pq.PolarKVCache(cfg, plan.n_units, 128, 0, capacity=T)
@@ -55,8 +56,13 @@ def _worker(rank, world, port, G, result_dir):
                     cache.prefill(torch.from_numpy(_keys(shape, layer, b, h, T)).cuda().unsqueeze(0),
                                   torch.from_numpy(vals[layer, b, h]).cuda().unsqueeze(0), unit_start=u)
         dec = sh.HeadShardedDecoder(cache, plan, gather="p2p")
-        got = [dec.step(q).float().cpu().numpy() for _ in range(2)]  # two eager steps
+        # four eager steps with different queries and no host barrier between
+        # them (the double-buffered gather keeps a fast rank from overwriting
+        # rows a slow rank has not read yet)
+        eager = [dec.step(qs[i]) for i in range(4)]
         torch.cuda.synchronize()
+        eager = [e.float().cpu().numpy() for e in eager]
+        got = []
         # CUDA-graph replay (the flags count publications, so replays stay in step)
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
@@ -65,6 +71,8 @@ def _worker(rank, world, port, G, result_dir):
         torch.cuda.current_stream().wait_stream(side)
         torch.cuda.synchronize()
         graph = torch.cuda.CUDAGraph()
+        dec.begin_step()
+        par = dec.peers.parity
         with torch.cuda.graph(graph):
             for layer in range(shape.layers):
                 dec.layer(layer, q[layer])
@@ -74,7 +82,7 @@ def _worker(rank, world, port, G, result_dir):
             dist.barrier()  # every rank has cleared its buffer before anyone writes again
             graph.replay()
             torch.cuda.synchronize()
-            got.append(dec.peers.out.float().cpu().numpy())
+            got.append(dec.peers.out[par].float().cpu().numpy())
             dist.barrier()
         # reference: the full cache (all heads) decoded locally, [L, B, Hkv] units
         full = pq.PolarKVCache(cfg, shape.layers * shape.batch * shape.kv_heads, 128, 0, capacity=T)
@@ -84,10 +92,16 @@ def _worker(rank, world, port, G, result_dir):
                     u = (layer * shape.batch + b) * shape.kv_heads + h
                     full.prefill(torch.from_numpy(_keys(shape, layer, b, h, T)).cuda().unsqueeze(0),
                                  torch.from_numpy(vals[layer, b, h]).cuda().unsqueeze(0), unit_start=u)
-        qu = q.reshape(shape.layers * shape.batch * shape.kv_heads, G, 128)
-        ref = full.decode(qu, out_dtype=torch.float32).reshape(shape.layers, shape.batch, shape.q_heads, 128)
-        ref = ref.cpu().numpy()
-        errs = [float(np.abs(g - ref).max() / max(1.0, np.abs(ref).max())) for g in got]
+        def ref_of(qq):
+            qu = qq.reshape(shape.layers * shape.batch * shape.kv_heads, G, 128)
+            r = full.decode(qu, out_dtype=torch.float32).reshape(shape.layers, shape.batch, shape.q_heads, 128)
+            return r.cpu().numpy()
+
+        def err(g, r):
+            return float(np.abs(g - r).max() / max(1.0, np.abs(r).max()))
+
+        ref = ref_of(q)
+        errs = [err(g, ref) for g in got] + [err(e, ref_of(qs[i])) for i, e in enumerate(eager)]
         np.save(os.path.join(result_dir, f"rank{rank}.npy"), np.array(errs))
         dist.barrier()
     finally:
