@@ -3,24 +3,32 @@
 Headline workload (BASELINE.json configs[1]): Llama-3.1-8B decode attention,
 all 32 layers, batch 16, 32K context, 32 query / 8 KV heads, d=128, m=4/n=4
 polar keys + bf16 values.  One step = one decode step over all 32 layers (per
-layer one fused LUT-attention launch over its 128 (sequence, kv-head) units
-plus the split merge, captured in a CUDA graph).  value = sequences advanced
-per second (tokens/s), whole job.
+layer one fused decode launch over its 128 (sequence, kv-head) units plus the
+split merge, captured in a CUDA graph).  value = sequences advanced per second
+(tokens/s), whole job.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--shard batch|heads] [--no-extras]
+                  [--shard batch|heads] [--no-extras] [--no-parity]
 
-Multi-GPU (torchrun, one process per GPU):
+Multi-GPU: one process per GPU.  Under torchrun the ranks come from the
+environment; ``--gpus N`` without WORLD_SIZE re-launches itself under
+torch.distributed.run with N ranks (ranks beyond the visible GPUs share them,
+over gloo, as a functional check of the N > 1 path).
   --shard batch (default)  each rank owns its own 16 sequences: units are
                            independent, no data-path collective -> "weak".
   --shard heads            configs[2]/[3] style: the fixed global batch is split
-                           by KV head; every layer all-gathers the head outputs
-                           over NCCL -> "strong".
-Time = max over ranks of the device-timed region.
+                           by KV head; the per-layer head-output gather is fused
+                           into the decode epilogue (peer stores) -> "strong".
+For N > 1 the line also carries configs[2] (m3n2, 128K, KV-head sharded over
+the N ranks) and configs[3] (70B shape, G = 8, KV-head sharded with the fused
+gather) measured the same way.  Time = max over ranks of the device-timed region.
 
-Extras (rank 0, 1 GPU, after the headline): configs[0] (small, latency),
-configs[2] at P=1 (128K ctx, m3n2), configs[3] per-GPU slice (70B head shape,
-one KV head of 8), configs[4] encoder slab.
+Value and e2e are timed interleaved over --reps repetitions (median reported,
+spread alongside).  After timing, a parity leg checks sampled units of the
+timed caches (every unit of layer 0 plus a random sample) against the oracle:
+codes bit-exact vs the correctly rounded C restatement, ties counted vs the
+numpy restatement of the reference, outputs vs softmax64 . V (oracle/parity.py;
+the oracle is the checker only, never on the timed path).
 """
 
 from __future__ import annotations
@@ -29,6 +37,8 @@ import argparse
 import json
 import math
 import os
+import socket
+import subprocess
 import sys
 import threading
 import time
@@ -40,6 +50,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "PolarQuant decode-attn tokens/s, Llama-3.1-8B heads @32K ctx; % HBM roofline"
+REF_DIR = ROOT / "baseline" / "_ref"  # the unmodified reference, pip-installed
 
 
 def parse():
@@ -47,6 +58,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--reps", type=int, default=3, help="interleaved value / e2e repetitions (median reported)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--shard", choices=["batch", "heads"], default="batch")
     ap.add_argument("--gather", choices=["p2p", "nccl"], default="p2p",
@@ -59,16 +71,22 @@ def parse():
     ap.add_argument("--m", type=int, default=4)
     ap.add_argument("--n", type=int, default=4)
     ap.add_argument("--page-tokens", type=int, default=256,
-                    help="tokens per cache page (decode per-launch rate vs page: 64 0.95, 128 0.98, 256 1.02, 512 1.03 at G=4; profiles/r01/page_size_sweep.md)")
+                    help="tokens per cache page (decode per-launch rate vs page: 64 0.95, 128 0.98, 256 1.02, "
+                         "512 1.03 at G=4; profiles/r01/page_size_sweep.md)")
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--no-extras", action="store_true", help="skip configs 1/3/4/5 side measurements")
+    ap.add_argument("--no-extras", action="store_true", help="skip the other configs' side measurements")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-parity", action="store_true", help="skip the parity leg")
+    ap.add_argument("--parity-sample", type=int, default=16,
+                    help="units checked beyond layer 0 (headline); extras check this many in total")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--sustain-seconds", type=float, default=2.5,
                     help="extra back-to-back decode after the timed region, reported as 'sustained' (0: skip)")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no timing claims)")
     ap.add_argument("--variant", choices=["auto", "lut", "dq"], default="auto",
                     help="scoring kernel of the fused decode (auto: the library's per-G choice)")
+    ap.add_argument("--values", choices=["bf16", "f32", "vq4"], default="bf16",
+                    help="value-cache treatment of the headline workload")
     return ap.parse_args()
 
 
@@ -79,8 +97,8 @@ def peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
-    return {"hbm_gbs": 6650.0, "source": "fallback"}
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json, copy bandwidth)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
 class ClockSampler:
@@ -144,36 +162,65 @@ class ClockSampler:
                 "reasons": sorted(n for b, n in self.REASONS.items() if bits & b), "samples": len(self.samples)}
 
 
-def unit_bytes(T: int, G: int, d: int, m: int, n: int, value_bits: int | None = None) -> int:
+def unit_bytes(T: int, G: int, d: int, m: int, n: int, values: str = "bf16") -> int:
     """Algorithmic HBM bytes of one (sequence, layer, kv-head) unit per decode
-    step: codes once per KV head, V once (bf16, or 4-bit codes +
-    fp32 (zp, scale) per token in the value-quantized mode), fp16 scales, bf16
-    q in / bf16 out for the G query heads."""
-    v = T * d * 2 if value_bits is None else T * (d * value_bits // 8 + 8)
+    step: codes once per KV head, V once (bf16 rows, fp32 rows,
+    or 4-bit codes + fp32 (zp, scale) per token), fp16 scales, bf16 q in /
+    bf16 out for the G query heads."""
+    v = {"bf16": T * d * 2, "f32": T * d * 4, "vq4": T * (d // 2 + 8)}[values]
     return T * (d // 2) * (m + n) // 8 + v + (d // 2) * 2 + 2 * G * d * 2
+
+
+def spread(xs) -> dict:
+    xs = sorted(float(x) for x in xs)
+    return {"median": float(np.median(xs)), "min": xs[0], "max": xs[-1], "n": len(xs)}
 
 
 # ------------------------------------------------------------- CPU baseline
 
 
-def _cpu_worker(args):
-    """One host core: build one (sequence, kv-head) unit with the reference
-    algorithm (numpy oracle port: prefill untimed -- the GPU step does not
-    prefill either), then repeat its decode -- G query heads of qk_scores +
-    attention_weights + softmax.V -- until ``seconds`` elapse."""
-    T, d, m, n, G, seed, seconds = args
-    from oracle import polar_oracle as po
+_CPU_UNIT = None
 
-    keys = po.synthetic_keys(T, d, seed=seed, outliers=(0, 1))
+
+def _cpu_init(T, d, m, n, G, seed, use_ref):
+    """Worker initializer: build one (sequence, kv-head) unit with the
+    reference's own PackedKVCache.prefill (untimed -- the GPU step does not
+    prefill either)."""
+    global _CPU_UNIT
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
     rng = np.random.default_rng([seed, 1])
     vals = rng.standard_normal((T, d)).astype(np.float32)
     q = rng.standard_normal((G, d)).astype(np.float32)
-    oc = po.OracleCache(m, n, po.HALF_SPLIT, 0)
-    oc.prefill(keys, vals)
+    if use_ref:
+        sys.path.insert(0, str(REF_DIR))
+        import polarquant as ref  # the unmodified reference
+
+        keys = ref.gen_synthetic_keys(ref.SyntheticConfig(T, d, outlier_channels=frozenset({0, 1}), seed=seed)).data
+        cache = ref.PackedKVCache(ref.QuantConfig(m, n), 0)
+        cache.prefill(keys, vals)
+        values = cache.values()
+
+        def decode():
+            for g in range(G):  # qk_scores + attention_weights, then the restated softmax . V
+                w = ref.attention_weights(ref.qk_scores(q[g], cache), 1.0 / math.sqrt(d))
+                _ = w @ values
+    else:
+        from oracle import polar_oracle as po
+
+        keys = po.synthetic_keys(T, d, seed=seed, outliers=(0, 1))
+        oc = po.OracleCache(m, n, po.HALF_SPLIT, 0)
+        oc.prefill(keys, vals)
+
+        def decode():
+            for g in range(G):
+                oc.attention(q[g], 1.0 / math.sqrt(d))
+    _CPU_UNIT = decode
+
+
+def _cpu_run(seconds):
     done, t0 = 0, time.perf_counter()
     while True:
-        for g in range(G):
-            oc.attention(q[g], 1.0 / math.sqrt(d))
+        _CPU_UNIT()
         done += 1
         el = time.perf_counter() - t0
         if el >= seconds:
@@ -193,31 +240,44 @@ def cpu_model() -> str:
     return platform.processor() or "unknown"
 
 
-def cpu_baseline(T, d, m, n, G, units_per_step, batch, seconds: float) -> dict:
-    """Reference CPU path on every host core (one process per core) for
-    ~``seconds`` of decode work each, extrapolated linearly to a full step."""
-    from concurrent.futures import ProcessPoolExecutor
+class CpuBaseline:
+    """The reference CPU path on every host core (one process per core, each
+    holding one prefilled unit), timed in bounded samples and extrapolated
+    linearly in units (the reference is linear in units and T, README.md:25-27)."""
 
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
-    cores = len(os.sched_getaffinity(0))
-    t0 = time.perf_counter()
-    with ProcessPoolExecutor(max_workers=cores) as ex:
-        res = list(ex.map(_cpu_worker, [(T, d, m, n, G, 10_001 + i, seconds) for i in range(cores)]))
-    wall = time.perf_counter() - t0
-    units_per_s = sum(k / el for k, el in res)
-    step_s = units_per_step / units_per_s
-    n_units = sum(k for k, _ in res)
-    return {
-        "value": batch / step_s,
-        "unit": "tokens/s",
-        "cores": cores,
-        "cpu_model": cpu_model(),
-        "kind": "port",
-        "sample": f"{n_units} unit-decodes ({G} query heads each, T={T}: qk_scores + attention_weights + "
-                  f"softmax.V of the numpy oracle port of the reference) on {cores} processes, {wall:.1f}s wall "
-                  f"incl. setup; rate extrapolated linearly to {units_per_step} units/step",
-        "sec_per_unit_1core": cores / units_per_s,
-    }
+    def __init__(self, T, d, m, n, G, units_per_step, batch):
+        from concurrent.futures import ProcessPoolExecutor
+
+        self.use_ref = (REF_DIR / "polarquant" / "__init__.py").exists()
+        self.cores = len(os.sched_getaffinity(0))
+        self.T, self.G, self.units_per_step, self.batch = T, G, units_per_step, batch
+        self.ex = ProcessPoolExecutor(max_workers=self.cores, initializer=_cpu_init,
+                                      initargs=(T, d, m, n, G, 10_001, self.use_ref))
+
+    def sample(self, seconds: float) -> dict:
+        t0 = time.perf_counter()
+        res = list(self.ex.map(_cpu_run, [seconds] * self.cores))
+        wall = time.perf_counter() - t0
+        units_per_s = sum(k / el for k, el in res)
+        step_s = self.units_per_step / units_per_s
+        n_units = sum(k for k, _ in res)
+        what = ("the unmodified reference (baseline/_ref: PackedKVCache.prefill untimed, qk_scores + "
+                "attention_weights + the restated softmax.V)" if self.use_ref else
+                "the numpy oracle port of the reference (baseline/_ref absent)")
+        return {
+            "value": self.batch / step_s,
+            "unit": "tokens/s",
+            "cores": self.cores,
+            "cpu_model": cpu_model(),
+            "kind": "reference" if self.use_ref else "port",
+            "sample": f"{n_units} unit-decodes ({self.G} query heads each, T={self.T}) of {what} on "
+                      f"{self.cores} processes in {wall:.1f}s wall; the rate is extrapolated linearly to the "
+                      f"{self.units_per_step} units of one step",
+            "sec_per_unit_1core": self.cores / units_per_s,
+        }
+
+    def close(self):
+        self.ex.shutdown()
 
 
 # ------------------------------------------------------------------- ours
@@ -227,10 +287,12 @@ class DecodeWorkload:
     """A multi-layer decode cache on one GPU plus its per-step launch sequence.
 
     layers x (batch x kv_heads) units, each with T tokens; one step runs every
-    layer's fused decode (optionally followed by the head-output gather)."""
+    layer's fused decode (with head sharding, fused with the head-output
+    gather).  ``keep`` lists local unit ids whose keys / values are kept (on
+    the device, bf16) for the parity leg."""
 
     def __init__(self, dev, *, layers, batch, hq, hkv, T, m, n, page_tokens, seed, plan=None, group=None,
-                 value_bits=None, gather="p2p"):
+                 values="bf16", gather="p2p", keep=()):
         import torch
 
         import paper_2502_00527_b200 as pq
@@ -241,20 +303,28 @@ class DecodeWorkload:
         self.plan, self.group = plan, group
         self.upl = plan.units_per_layer if plan is not None else batch * hkv
         self.batch, self.hq = batch, hq
+        self.values = values
         cfg = pq.QuantConfig(m, n)
-        self.value_bits = value_bits
         self.cache = pq.PolarKVCache(cfg, layers * self.upl, 128, 0, capacity=T, page_tokens=page_tokens,
-                                     value_dtype=torch.bfloat16, device=dev, value_bits=value_bits)
+                                     value_dtype=torch.float32 if values == "f32" else torch.bfloat16, device=dev,
+                                     value_bits=4 if values == "vq4" else None)
         syn = pq.SyntheticConfig(T, 128, outlier_channels=frozenset({0, 1}))
         chunk = max(1, min(self.upl, (1 << 31) // (T * 128 * 2)))  # <= 2 GB bf16 staging per tensor
+        keep = set(int(u) for u in keep)
+        self.kept: dict[int, tuple] = {}
         for layer in range(layers):
             for u0 in range(0, self.upl, chunk):
                 k = min(chunk, self.upl - u0)
                 s = (seed * 1000 + layer) * 7919 + u0 + 1
                 keys = pq.synthetic_keys_device(syn, k, dtype=torch.bfloat16, device=dev, seed=s)
                 vals = pq.normal_device((k, T, 128), s + 1, dtype=torch.bfloat16, device=dev)
-                self.cache.prefill(keys, vals, unit_start=layer * self.upl + u0, check=(layer == 0 and u0 == 0))
+                base = layer * self.upl + u0
+                self.cache.prefill(keys, vals, unit_start=base, check=False)
+                for j in range(k):
+                    if base + j in keep:
+                        self.kept[base + j] = (keys[j].clone(), vals[j].clone())
                 del keys, vals
+        self.cache.check()  # any non-finite key / scale overflow in any chunk raises here
         self.q = pq.normal_device((layers, self.upl, self.G, 128), 424242 + seed, dtype=torch.bfloat16, device=dev)
         self.out = torch.empty((layers, self.upl, self.G, 128), dtype=torch.bfloat16, device=dev)
         self.views = [self.cache.view(i * self.upl, (i + 1) * self.upl) for i in range(layers)]
@@ -272,10 +342,12 @@ class DecodeWorkload:
         torch.cuda.synchronize(dev)
         self.base_flags = 0  # PQB_DECODE_* bits added to every launch (kernel-variant probes)
 
-    def step(self, flags: int = 0):
+    # ---- one step: every layer's decode (+ gather)
+    def step(self, flags: int = 0, parity: int | None = None):
         if self.peers is not None:
+            par = self.peers.next_step() if parity is None else parity
             for i in range(self.L):
-                self.views[i].decode_peer(self.q[i], self.peers.descriptor(i), max_tokens=self.T)
+                self.views[i].decode_peer(self.q[i], self.peers.descriptor(i, par), max_tokens=self.T)
             for i in range(self.L):
                 self.peers.wait(i)
             return
@@ -297,17 +369,30 @@ class DecodeWorkload:
         return self.L * int(_lib.load().pqb_decode_launches(self.upl, self.G, self.T, self.base_flags))
 
     def bytes_per_launch(self) -> int:
-        return self.upl * unit_bytes(self.T, self.G, 128, self.m, self.n, self.value_bits)
+        return self.upl * unit_bytes(self.T, self.G, 128, self.m, self.n, self.values)
 
     def capture(self, fn):
+        """CUDA graph of fn; with the peer gather two graphs (the gathered
+        buffer alternates between steps), replayed alternately."""
         torch = self.torch
         with torch.cuda.stream(self.stream):
-            fn()
+            fn() if self.peers is None else fn(parity=0)
         torch.cuda.synchronize(self.dev)
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=self.stream):
-            fn()
-        return g.replay
+        if self.peers is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                fn()
+            return g.replay
+        graphs = []
+        for par in (0, 1):
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                fn(parity=par)
+            graphs.append(g)
+        def replay():  # every step (graph or eager) flips the buffer: the double-buffer contract
+            graphs[self.peers.next_step()].replay()
+
+        return replay
 
     def timed(self, fn, steps: int, warmup: int, dist=None) -> float:
         torch = self.torch
@@ -327,193 +412,355 @@ class DecodeWorkload:
         torch.cuda.synchronize(self.dev)
         ms = e0.elapsed_time(e1) / steps
         if dist:
-            on_dev = dist.get_backend() == "nccl"
-            t = torch.tensor([ms], device=self.dev if on_dev else "cpu", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = float(t.item())
+            ms = max_over_ranks(ms, dist, self.dev)
         return ms
 
+    # ---- end to end through the public API with pinned host buffers
+    def e2e_fn(self):
+        """Per step: H2D of every layer's queries (layer 0 first, the rest on a
+        copy stream while layer 0 decodes), the per-layer public decode calls
+        (decode / decode_peer + wait), and D2H of every layer's output on a
+        copy stream as soon as the layer is done; the step ends when the last
+        output is on the host."""
+        torch = self.torch
+        dev, L = self.dev, self.L
+        q_host = self.q.cpu().pin_memory()
+        src = self.peers.out[0] if self.peers is not None else self.out
+        o_host = torch.empty(src.shape, dtype=src.dtype).pin_memory()
+        q_dev = torch.empty_like(self.q)
+        h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+        ev_q = torch.cuda.Event()
+        ev_l = [torch.cuda.Event() for _ in range(L)]
+
+        def e2e_step():
+            main = torch.cuda.current_stream(dev)
+            q_dev[0].copy_(q_host[0], non_blocking=True)
+            if L > 1:
+                h2d_s.wait_stream(main)  # the previous step is done with q_dev
+                with torch.cuda.stream(h2d_s):
+                    q_dev[1:].copy_(q_host[1:], non_blocking=True)
+                    ev_q.record(h2d_s)
+            par = self.peers.next_step() if self.peers is not None else None
+            for i in range(L):
+                if i == 1:
+                    main.wait_event(ev_q)
+                if self.peers is not None:
+                    self.views[i].decode_peer(q_dev[i], self.peers.descriptor(i, par), max_tokens=self.T)
+                    self.peers.wait(i)
+                    out_i = self.peers.out[par, i]
+                else:
+                    self.views[i].decode(q_dev[i], out=self.out[i], max_tokens=self.T)
+                    out_i = self.out[i]
+                ev_l[i].record(main)
+                d2h_s.wait_event(ev_l[i])
+                with torch.cuda.stream(d2h_s):
+                    o_host[i].copy_(out_i, non_blocking=True)
+            main.wait_stream(d2h_s)  # consumed before the next step may overwrite (double-buffer contract)
+
+        return e2e_step, q_host.numel() * q_host.element_size(), o_host.numel() * o_host.element_size()
+
+    # ---- parity leg (after timing; oracle/parity.py is the checker)
+    def parity_jobs(self, units):
+        """check_unit kwargs for local units from the last step's outputs."""
+        jobs = []
+        par = self.peers.parity if self.peers is not None else None
+        for u in units:
+            keys, vals = self.kept[u]
+            layer, j = divmod(u, self.upl)
+            if self.peers is not None:
+                p = self.plan
+                b, h = p.b0 + j // p.kv_heads, p.h0 + j % p.kv_heads
+                out = self.peers.out[par, layer, b, h * self.G:(h + 1) * self.G]
+            else:
+                out = self.out[layer, j]
+            a, r = self.cache.code_arrays(u)
+            # 4-bit values: the reference's dequantized rows (values(), bit-identical to
+            # quantize_uniform / dequantize_uniform, tests/test_oracle_golden.py)
+            v = self.cache.values_f32(u) if self.values == "vq4" else vals.float()
+            jobs.append(dict(keys=keys.float().cpu().numpy(), s16_gpu=self.cache.scales16[u].cpu().numpy(),
+                             angle_gpu=a.cpu().numpy(), radius_gpu=r.cpu().numpy(), m=self.m, n=self.n,
+                             q=self.q[layer, j].float().cpu().numpy(), values=v.cpu().numpy(),
+                             out=out.float().cpu().numpy(), out_bf16=True))
+        return jobs
+
     def free(self):
-        del self.cache, self.q, self.out, self.views
+        del self.cache, self.q, self.out, self.views, self.kept
+        self.peers = None
         self.torch.cuda.empty_cache()
 
 
-def measure_workload(w: DecodeWorkload, steps: int, warmup: int, graph: bool = True) -> dict:
-    """Step time (graph) + attention-kernel-only time per launch + roofline."""
-    from paper_2502_00527_b200 import _lib
+def max_over_ranks(x: float, dist, dev) -> float:
+    import torch
 
-    run = w.capture(w.step) if graph else w.step
-    run_attn = w.capture(lambda: w.step(_lib.PQB_DECODE_NO_COMBINE)) if graph else (
-        lambda: w.step(_lib.PQB_DECODE_NO_COMBINE))
-    ms = w.timed(run, steps, warmup)
-    ms_attn = w.timed(run_attn, max(3, steps // 2), 2) / w.L
-    pk = peaks()
-    algo = w.bytes_per_launch()
-    return {"ms_per_step": ms, "tokens_per_s": w.batch / (ms * 1e-3), "avg_launch_ms": ms_attn,
-            "achieved_gbs": algo / (ms_attn * 1e-3) / 1e9, "frac": algo / (ms_attn * 1e-3) / 1e9 / pk["hbm_gbs"],
-            "step_frac": w.L * algo / (ms * 1e-3) / 1e9 / pk["hbm_gbs"]}
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([x], device=dev if on_dev else "cpu", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def parity_leg(w: DecodeWorkload, units, run, dist=None) -> dict:
+    """One more regular step (graph replay), then the oracle checks of the
+    sampled units on host threads; summaries of all ranks merged on rank 0."""
+    from oracle import parity
+
+    t0 = time.perf_counter()
+    with w.torch.cuda.stream(w.stream):
+        run()
+    w.torch.cuda.synchronize(w.dev)
+    results = parity.check_many(w.parity_jobs(units))
+    summ = parity.summarize(results)
+    summ["seconds"] = time.perf_counter() - t0
+    if dist:
+        allsum = [None] * dist.get_world_size()
+        dist.all_gather_object(allsum, summ)
+        merged = dict(allsum[0])
+        for k in ("units", "codes_checked", "scale_mismatches", "exact_code_mismatches", "numpy_ties",
+                  "numpy_angle_ties", "numpy_radius_ties", "non_tie_mismatches"):
+            merged[k] = sum(s[k] for s in allsum)
+        merged["tie_rate"] = merged["numpy_ties"] / max(1, merged["codes_checked"])
+        merged["max_out_rel_err"] = max(s["max_out_rel_err"] for s in allsum)
+        merged["out_within_tol"] = all(s["out_within_tol"] for s in allsum)
+        merged["ranks"] = len(allsum)
+        summ = merged
+    summ["passed"] = parity.passed(summ)
+    return summ
+
+
+def sample_units(upl: int, layers: int, extra: int, seed: int, all_layer0: bool = True) -> list[int]:
+    rng = np.random.default_rng(seed)
+    base = list(range(upl)) if all_layer0 else []
+    pool = np.arange(upl if all_layer0 else 0, layers * upl)
+    more = rng.choice(pool, size=min(extra, pool.size), replace=False).tolist() if pool.size else []
+    return sorted(set(base + [int(u) for u in more]))
 
 
 def run_ours(a, rank: int, world: int, dist) -> dict | None:
     import torch
 
-    from paper_2502_00527_b200 import sharding
+    from paper_2502_00527_b200 import _lib, sharding
 
-    dev = torch.device("cuda", torch.cuda.current_device() if world > 1 else int(os.environ.get("LOCAL_RANK", 0)))
-    torch.cuda.set_device(dev)
+    dev = torch.device("cuda", torch.cuda.current_device())
     G = a.hq // a.hkv
     plan = None
     batch = a.batch
     if a.shard == "heads" and world > 1:
         shape = sharding.DecodeShape(a.layers, a.batch, a.hq, a.hkv)
         plan = sharding.head_shard(shape, world, rank)
+    upl = plan.units_per_layer if plan is not None else a.batch * a.hkv
+    keep = [] if a.no_parity or a.profile else sample_units(upl, a.layers, a.parity_sample, 77 + rank)
     w = DecodeWorkload(dev, layers=a.layers, batch=batch, hq=a.hq, hkv=a.hkv, T=a.ctx, m=a.m, n=a.n,
-                       page_tokens=a.page_tokens, seed=rank, plan=plan, gather=a.gather)
-    from paper_2502_00527_b200 import _lib as _l
-
-    w.base_flags = {"auto": 0, "lut": _l.PQB_DECODE_LUT, "dq": _l.PQB_DECODE_DQ}[a.variant]
+                       page_tokens=a.page_tokens, seed=rank, plan=plan, gather=a.gather, values=a.values,
+                       keep=keep, group=None)
+    w.base_flags = {"auto": 0, "lut": _lib.PQB_DECODE_LUT, "dq": _lib.PQB_DECODE_DQ}[a.variant]
     if a.profile:
         with torch.cuda.stream(w.stream):
             for _ in range(max(1, a.steps)):
                 w.step()
         torch.cuda.synchronize(dev)
         return None
-    from paper_2502_00527_b200 import _lib
 
     run = w.step if a.no_graph else w.capture(w.step)
+    e2e_step, h2d, d2h = w.e2e_fn()
+    ms_v, ms_e = [], []
     with ClockSampler(dev) as clk:
-        ms_step = w.timed(run, a.steps, a.warmup, dist)
-    run_attn = (lambda: w.step(_lib.PQB_DECODE_NO_COMBINE))
-    run_attn = run_attn if a.no_graph else w.capture(run_attn)
-    ms_attn_layer = w.timed(run_attn, max(3, a.steps // 2), 2, dist) / a.layers
+        for rep in range(max(1, a.reps)):  # value and e2e interleaved
+            ms_v.append(w.timed(run, a.steps, a.warmup if rep == 0 else 2, dist))
+            ms_e.append(w.timed(e2e_step, a.steps, a.warmup if rep == 0 else 2, dist))
+    ms_step, ms_e2e = float(np.median(ms_v)), float(np.median(ms_e))
 
-    # ---- e2e through the public API with host buffers (pinned), per step:
-    #      H2D of every layer's queries, per-layer decode calls, D2H of outputs.
-    #      The copies overlap the decode the way a serving loop would issue
-    #      them: layer 0's queries first, the other layers' on a copy stream
-    #      while layer 0 decodes; all but the last layer's outputs leave on a
-    #      copy stream while the last layer decodes.
-    q_host = w.q.cpu().pin_memory()
-    o_host = torch.empty(w.out.shape, dtype=w.out.dtype).pin_memory()
-    q_dev = torch.empty_like(w.q)
-    h2d_s, d2h_s = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
-    ev_q, ev_o = torch.cuda.Event(), torch.cuda.Event()
-    L = a.layers
+    # kernel-only rate of the dominant launch (roofline): the same step with
+    # the split merge skipped (PQB_DECODE_NO_COMBINE) -- the attention kernel's
+    # launches alone, stated as such; step_frac (below) includes the merge
+    if w.peers is None:
+        run_attn = (lambda: w.step(_lib.PQB_DECODE_NO_COMBINE))
+        run_attn = run_attn if a.no_graph else w.capture(run_attn)
+        ms_attn_layer = w.timed(run_attn, max(3, a.steps // 2), 2, dist) / a.layers
+    else:
+        ms_attn_layer = None
 
-    def e2e_step():
-        main = torch.cuda.current_stream(dev)
-        q_dev[0].copy_(q_host[0], non_blocking=True)
-        if L > 1:
-            h2d_s.wait_stream(main)  # the previous step is done with q_dev
-            with torch.cuda.stream(h2d_s):
-                q_dev[1:].copy_(q_host[1:], non_blocking=True)
-                ev_q.record(h2d_s)
-        for i in range(L):
-            if i == 1:
-                main.wait_event(ev_q)
-            w.views[i].decode(q_dev[i], out=w.out[i], max_tokens=a.ctx)
-            if i == L - 2:
-                ev_o.record(main)
-                d2h_s.wait_event(ev_o)
-                with torch.cuda.stream(d2h_s):
-                    o_host[:L - 1].copy_(w.out[:L - 1], non_blocking=True)
-        o_host[L - 1].copy_(w.out[L - 1], non_blocking=True)
-        if L > 1:
-            main.wait_stream(d2h_s)  # the step ends when every output is on the host
-
-    ms_e2e = w.timed(e2e_step, max(3, a.steps // 2), 2, dist)
+    parity = parity_leg(w, keep, run, dist) if keep else None
 
     # ---- sustained: the same graph step back to back for a few seconds (the
-    #      board reaches its 1000 W cap within ~0.3 s; profiles/r01/power_probe.md);
-    #      reported beside the K-step value, not instead of it
+    #      board reaches its 1000 W cap within ~0.3 s; profiles/r01/power_probe.md)
     sustained = None
     if a.sustain_seconds > 0 and not a.no_graph:
-        import time as _t
-
         with ClockSampler(dev) as sclk:
-            t_end = _t.time() + a.sustain_seconds
+            t_end = time.time() + a.sustain_seconds
             chunks = []
-            while _t.time() < t_end:
+            while time.time() < t_end:
                 chunks.append(w.timed(run, 8, 0))
         tail = chunks[len(chunks) // 2:] or chunks
         ms_sus = sum(tail) / len(tail)
-        sustained = {"seconds": a.sustain_seconds, "ms_per_step": ms_sus,
-                     "value": (a.batch * world if a.shard == "batch" else a.batch) / (ms_sus * 1e-3),
-                     "note": "second half of a back-to-back run of the timed step",
-                     "clocks": sclk.summary()}
+        gb = a.batch * world if a.shard == "batch" else a.batch
+        sustained = {"seconds": a.sustain_seconds, "ms_per_step": ms_sus, "value": gb / (ms_sus * 1e-3),
+                     "note": "second half of a back-to-back run of the timed step", "clocks": sclk.summary()}
     algo = w.bytes_per_launch()
     pk = peaks()
-    achieved = algo / (ms_attn_layer * 1e-3) / 1e9
     global_batch = a.batch * world if a.shard == "batch" else a.batch
+    step_frac = a.layers * algo / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"]
+    kern = (f"decode_fast_kernel<G={G},M={a.m},N={a.n}> (LUT gather)" if a.variant == "lut" or G not in (4, 8)
+            else f"decode_dq_kernel<G={G},M={a.m},N={a.n}> (product-table gather + tensor-core QK, "
+                 f"{'CUDA-core fp32' if a.values == 'f32' else 'tensor-core'} P.V)")
+    if ms_attn_layer is not None:
+        achieved = algo / (ms_attn_layer * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"],
+                "frac_basis": "attention kernel launches alone: the per-layer launch timed with the split merge "
+                              "skipped (PQB_DECODE_NO_COMBINE), CUDA events on the launch stream; step_frac "
+                              "includes the merge and every launch of the step"}
+    else:
+        achieved = a.layers * algo / (ms_step * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "frac_basis": "whole step (fused decode + gather launches)"}
+    roof.update({
+        "peak_source": pk["source"],
+        "frac_vs_8tbs_nameplate": achieved / 8000.0,  # SURVEY 8(d) asks for both denominators
+        "kernel": kern,
+        "algorithmic_bytes_per_launch": algo,
+        "bytes_formula": "per unit T*(d/2)*(m+n)/8 codes + V + (d/2)*2 scales + 2*G*d*2 q/out (SURVEY 8(d))",
+        "avg_launch_ms": ms_attn_layer,
+        "step_frac": step_frac,
+        "traffic": ncu_traffic() if a.values == "bf16" and a.m == 4 and a.n == 4 and G == 4 else None,
+    })
     res = {
         "ms_per_step": ms_step,
         "value": global_batch / (ms_step * 1e-3),
+        "value_reps": spread(global_batch / (m * 1e-3) for m in ms_v),
         "e2e_ms": ms_e2e,
         "e2e_value": global_batch / (ms_e2e * 1e-3),
-        "h2d": q_host.numel() * q_host.element_size(),
-        "d2h": o_host.numel() * o_host.element_size(),
-        "roofline": {
-            "bound": "hbm",
-            "achieved": achieved,
-            "peak": pk["hbm_gbs"],
-            "unit": "GB/s",
-            "frac": achieved / pk["hbm_gbs"],
-            "peak_source": pk["source"],
-            "frac_vs_8tbs_nameplate": achieved / 8000.0,  # SURVEY 8(d) asks for both denominators
-            "kernel": (f"decode_fast_kernel<G={G},M={a.m},N={a.n}> (LUT gather" if a.variant == "lut" or G not in (4, 8)
-                       else f"decode_dq_kernel<G={G},M={a.m},N={a.n}> (product-table gather + tensor-core QK")
-                      + "; persistent; timed with the in-kernel split merge disabled)",
-            "algorithmic_bytes_per_launch": algo,
-            "avg_launch_ms": ms_attn_layer,
-            "step_frac": a.layers * algo / (ms_step * 1e-3) / 1e9 / pk["hbm_gbs"],
-            "traffic": ncu_traffic(),
-        },
+        "e2e_reps": spread(global_batch / (m * 1e-3) for m in ms_e),
+        "h2d": h2d,
+        "d2h": d2h,
+        "roofline": roof,
         "clocks": clk.summary(),
         "sustained": sustained,
         "gpu_launches": a.steps * w.launches_per_step(),
         "global_batch": global_batch,
+        "parity": parity,
     }
     w.free()
     del w
     torch.cuda.empty_cache()
-    if rank == 0 and world == 1 and not a.no_extras:
-        res["extras"] = run_extras(dev, a)
+    if not a.no_extras:
+        res["extras"] = run_extras(dev, a, rank, world, dist)
     return res
 
 
-def run_extras(dev, a) -> dict:
-    """Side measurements of the other BASELINE configs on one GPU."""
+def measure_workload(w: DecodeWorkload, steps: int, warmup: int, dist=None, graph: bool = True) -> dict:
+    """Step time (graph) + attention-kernel-only time per launch + roofline."""
+    from paper_2502_00527_b200 import _lib
+
+    run = w.capture(w.step) if graph else w.step
+    ms = w.timed(run, steps, warmup, dist)
+    pk = peaks()
+    algo = w.bytes_per_launch()
+    r = {"ms_per_step": ms, "step_frac": w.L * algo / (ms * 1e-3) / 1e9 / pk["hbm_gbs"],
+         "gpu_launches_per_step": w.launches_per_step()}
+    if w.peers is None:
+        run_attn = w.capture(lambda: w.step(_lib.PQB_DECODE_NO_COMBINE)) if graph else (
+            lambda: w.step(_lib.PQB_DECODE_NO_COMBINE))
+        ms_attn = w.timed(run_attn, max(3, steps // 2), 2, dist) / w.L
+        r.update({"avg_launch_ms": ms_attn, "achieved_gbs": algo / (ms_attn * 1e-3) / 1e9,
+                  "frac": algo / (ms_attn * 1e-3) / 1e9 / pk["hbm_gbs"],
+                  "frac_basis": "kernel only (split merge skipped)"})
+    r["_run"] = run
+    return r
+
+
+def run_extras(dev, a, rank: int, world: int, dist) -> dict:
+    """The other BASELINE configs.  N = 1: per-GPU side measurements on rank 0.
+    N > 1: configs[2] and configs[3] KV-head sharded over the N ranks with the
+    fused head-output gather, timed as the max over ranks."""
     import torch
 
+    from paper_2502_00527_b200 import sharding
+
     out = {}
+    if world == 1:
+        specs = {
+            "configs[0]_L1_B1_4K_m4n4": dict(layers=1, batch=1, hq=32, hkv=8, T=4096, m=4, n=4),
+            "configs[2]_P1_L32_B8_128K_m3n2": dict(layers=32, batch=8, hq=32, hkv=8, T=131072, m=3, n=2),
+            "configs[3]_per_gpu_L80_B32_32K_G8_1kvhead": dict(layers=80, batch=32, hq=8, hkv=1, T=32768, m=4, n=4),
+            # SURVEY 8(f) #2: configs[1] with the reference's value-quantization mode
+            # (PackedKVCache(quantize_values=True, value_bits=4)) read inside the kernel
+            "configs[1]_vq4_values": dict(layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, values="vq4"),
+            # the reference's default value cache: full-precision fp32 rows (kv_cache.py:8-9, :209)
+            "configs[1]_f32_values": dict(layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, values="f32"),
+        }
+        parity_of = {"configs[2]_P1_L32_B8_128K_m3n2", "configs[3]_per_gpu_L80_B32_32K_G8_1kvhead",
+                     "configs[1]_f32_values", "configs[1]_vq4_values"}
+        for name, s in specs.items():
+            try:
+                upl = s["batch"] * s["hkv"]
+                keep = (sample_units(upl, s["layers"], max(1, a.parity_sample // 2), 5, all_layer0=False)
+                        if name in parity_of and not a.no_parity else [])
+                w = DecodeWorkload(dev, page_tokens=a.page_tokens, seed=7, keep=keep, **s)
+                r = measure_workload(w, steps=max(3, a.steps // 2), warmup=2)
+                r["tokens_per_s"] = s["batch"] / (r["ms_per_step"] * 1e-3)
+                r["bytes_per_step"] = w.L * w.bytes_per_launch()
+                run = r.pop("_run")
+                if keep:
+                    r["parity"] = parity_leg(w, keep, run)
+                w.free()
+                del w
+                torch.cuda.empty_cache()
+                out[name] = r
+            except Exception as exc:  # report, never hide the headline
+                out[name] = {"error": f"{type(exc).__name__}: {exc}"}
+        try:
+            out["configs[1]_scores_only"] = scores_bench(dev, a)
+        except Exception as exc:
+            out["configs[1]_scores_only"] = {"error": f"{type(exc).__name__}: {exc}"}
+        try:
+            out["configs[4]_encode"] = encode_bench(dev, a)
+        except Exception as exc:
+            out["configs[4]_encode"] = {"error": f"{type(exc).__name__}: {exc}"}
+        return out
+    # N > 1: the configs whose layers span GPUs (KV-head sharding + fused gather)
+    per_gpu_budget = 0.8 * torch.cuda.mem_get_info(dev)[1] / max(1, ranks_per_device(world))
     specs = {
-        "configs[0]_L1_B1_4K_m4n4": dict(layers=1, batch=1, hq=32, hkv=8, T=4096, m=4, n=4),
-        "configs[2]_P1_L32_B8_128K_m3n2": dict(layers=32, batch=8, hq=32, hkv=8, T=131072, m=3, n=2),
-        "configs[3]_per_gpu_L80_B32_32K_G8_1kvhead": dict(layers=80, batch=32, hq=8, hkv=1, T=32768, m=4, n=4),
-        # SURVEY 8(f) #2: configs[1] with the reference's value-quantization mode
-        # (PackedKVCache(quantize_values=True, value_bits=4)) read inside the kernel
-        "configs[1]_vq4_values": dict(layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, value_bits=4),
+        f"configs[2]_P{world}_L32_B8_128K_m3n2_kvhead_sharded": dict(layers=32, batch=8, hq=32, hkv=8, T=131072,
+                                                                      m=3, n=2),
+        f"configs[3]_P{world}_L80_B32_32K_G8_kvhead_sharded": dict(layers=80, batch=32, hq=64, hkv=8, T=32768,
+                                                                    m=4, n=4),
     }
     for name, s in specs.items():
         try:
-            w = DecodeWorkload(dev, page_tokens=a.page_tokens, seed=7, **s)
-            r = measure_workload(w, steps=max(3, a.steps // 2), warmup=2)
-            r["bytes_per_step"] = w.L * w.bytes_per_launch()
+            shape = sharding.DecodeShape(s["layers"], s["batch"], s["hq"], s["hkv"])
+            plan = sharding.head_shard(shape, world, rank)
+            per_unit = unit_bytes(s["T"], s["hq"] // s["hkv"], 128, s["m"], s["n"])
+            layers = s["layers"]
+            fit = int(per_gpu_budget // (plan.units_per_layer * per_unit))
+            if fit < layers:  # more ranks than GPUs: fewer layers, stated in the line
+                layers = max(1, fit)
+                shape = sharding.DecodeShape(layers, s["batch"], s["hq"], s["hkv"])
+                plan = sharding.head_shard(shape, world, rank)
+            keep = [] if a.no_parity else sample_units(plan.units_per_layer, layers, 2, 9 + rank, all_layer0=False)
+            w = DecodeWorkload(dev, layers=layers, batch=s["batch"], hq=s["hq"], hkv=s["hkv"], T=s["T"], m=s["m"],
+                               n=s["n"], page_tokens=a.page_tokens, seed=11 + rank, plan=plan, gather="p2p",
+                               keep=keep)
+            r = measure_workload(w, steps=max(3, a.steps // 2), warmup=2, dist=dist)
+            run = r.pop("_run")
+            r["layers"] = layers
+            r["tokens_per_s"] = s["batch"] / (r["ms_per_step"] * 1e-3)
+            r["tokens_per_s_full_depth"] = s["batch"] / (r["ms_per_step"] * s["layers"] / layers * 1e-3)
+            r["scaling"] = "strong (fixed global batch split by KV head)"
+            r["bytes_per_step_per_gpu"] = w.L * w.bytes_per_launch()
+            if keep:
+                r["parity"] = parity_leg(w, keep, run, dist)
             w.free()
             del w
             torch.cuda.empty_cache()
             out[name] = r
-        except Exception as exc:  # report, never hide the headline
+        except Exception as exc:
             out[name] = {"error": f"{type(exc).__name__}: {exc}"}
-    try:
-        out["configs[1]_scores_only"] = scores_bench(dev, a)
-    except Exception as exc:
-        out["configs[1]_scores_only"] = {"error": f"{type(exc).__name__}: {exc}"}
-    try:
-        out["configs[4]_encode"] = encode_bench(dev, a)
-    except Exception as exc:
-        out["configs[4]_encode"] = {"error": f"{type(exc).__name__}: {exc}"}
     return out
+
+
+def ranks_per_device(world: int) -> int:
+    import torch
+
+    return max(1, math.ceil(world / max(1, torch.cuda.device_count())))
 
 
 def ncu_traffic():
@@ -576,8 +823,9 @@ def encode_bench(dev, a) -> dict:
     flags = torch.zeros(1, dtype=torch.int32, device=dev)
     ws = torch.empty(U * 64, dtype=torch.int64, device=dev)
     pk = peaks()
-    res = {"workload": f"{U} units x {T} tokens bf16 keys (configs[4] slab; scales + encode + pack)"}
-    for m, n in [(4, 4), (3, 2), (2, 4)]:
+    res = {"workload": f"{U} units x {T} tokens bf16 keys (configs[4] slab; scales + encode + pack)",
+           "inputs_vs_l2": "8.6 GB of keys per pass >> 126 MB L2"}
+    for m, n in [(4, 4), (3, 2), (2, 4), (2, 2), (3, 4), (4, 2)]:
         cfg = pq.QuantConfig(m, n)
         cache = pq.PolarKVCache(cfg, U, d, 0, capacity=T, page_tokens=256, value_dtype=torch.bfloat16, device=dev)
 
@@ -610,51 +858,80 @@ def encode_bench(dev, a) -> dict:
 # ------------------------------------------------------------------- main
 
 
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def maybe_spawn(a) -> None:
+    """``--gpus N`` outside torchrun: run this script under torch.distributed.run
+    with N ranks (one process per GPU) and exit with its status."""
+    if a.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    sys.exit(subprocess.run(cmd).returncode)
+
+
+def config_of(a, world: int, heads: bool) -> dict:
+    return {"workload": "configs[1]: Llama-3.1-8B heads (32 Q / 8 KV, d=128), 32 layers, batch 16/GPU, 32K ctx, "
+                        f"m=4 angle / n=4 radius bits, {a.values} V; one step = one decode step over all layers",
+            "layers": a.layers, "batch_per_gpu": a.batch, "ctx": a.ctx,
+            "global_batch": a.batch * world if not heads else a.batch,
+            "q_heads": a.hq, "kv_heads": a.hkv, "head_dim": 128, "angle_bits": a.m, "radius_bits": a.n,
+            "values": a.values, "page_tokens": a.page_tokens,
+            "parallelism": (f"kv-head sharded x{world} + per-layer head gather "
+                            + ("fused into the decode epilogue (peer stores over NVLink)" if a.gather == "p2p"
+                               else "(NCCL all-gather)") if heads
+                            else f"batch-sharded x{world} (no collective)"),
+            "l2": "inputs (43 GB cache per GPU) >> 126 MB L2; no flush needed"}
+
+
 def main() -> None:
     a = parse()
+    maybe_spawn(a)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     dist = None
+    import torch
+
+    ndev = max(1, torch.cuda.device_count()) if torch.cuda.is_available() else 1
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if torch.cuda.is_available():
+        torch.cuda.set_device(int(os.environ.get("PQB_BENCH_DEVICE", local % ndev)))
     if world > 1:
-        import torch
         import torch.distributed as tdist
 
-        # PQB_BENCH_DEVICE / PQB_BENCH_BACKEND: run the N > 1 path as N ranks on
-        # one GPU over gloo (a smoke test of the multi-rank code on a 1-GPU box)
-        dev_override = os.environ.get("PQB_BENCH_DEVICE")
-        torch.cuda.set_device(int(dev_override) if dev_override is not None else int(os.environ.get("LOCAL_RANK", 0)))
-        tdist.init_process_group(os.environ.get("PQB_BENCH_BACKEND", "nccl"))
+        # NCCL needs one GPU per rank; with more ranks than GPUs (a functional
+        # check on a small box) the host-side reductions run over gloo -- the
+        # data path has no collective in either case
+        backend = os.environ.get("PQB_BENCH_BACKEND", "nccl" if world <= ndev else "gloo")
+        tdist.init_process_group(backend)
         dist = tdist
     G = a.hq // a.hkv
-    upl = a.batch * a.hkv
-    units_per_step = a.layers * upl
     heads = a.shard == "heads" and world > 1
-    config = {"workload": "configs[1]: Llama-3.1-8B heads (32 Q / 8 KV, d=128), 32 layers, batch 16/GPU, 32K ctx, "
-                          "m=4 angle / n=4 radius bits, bf16 V; one step = one decode step over all layers",
-              "layers": a.layers, "batch_per_gpu": a.batch if not heads else a.batch, "ctx": a.ctx,
-              "global_batch": a.batch * world if not heads else a.batch,
-              "q_heads": a.hq, "kv_heads": a.hkv, "head_dim": 128, "angle_bits": a.m, "radius_bits": a.n,
-              "page_tokens": a.page_tokens,
-              "parallelism": (f"kv-head sharded x{world} + per-layer head gather "
-                              + ("fused into the decode epilogue (peer stores over NVLink)" if a.gather == "p2p"
-                                 else "(NCCL all-gather)") if heads
-                              else f"batch-sharded x{world} (no collective)"),
-              "l2": "inputs (43 GB cache per GPU) >> 126 MB L2; no flush needed"}
+    config = config_of(a, world, heads)
+    units_per_step = a.layers * a.batch * a.hkv
 
     if a.impl == "reference":
         if rank == 0:
+            cb = CpuBaseline(a.ctx, 128, a.m, a.n, G, units_per_step, a.batch)
             steps = []
+            per = max(1.0, a.cpu_seconds / 5)
             for i in range(a.warmup + a.steps):
-                cb = cpu_baseline(a.ctx, 128, a.m, a.n, G, units_per_step, a.batch,
-                                  seconds=max(1.0, a.cpu_seconds / 5))
+                s = cb.sample(per)
                 if i >= a.warmup:
-                    steps.append(cb)
-            v = float(np.mean([s["value"] for s in steps]))
+                    steps.append(s)
+            cb.close()
+            v = float(np.median([s["value"] for s in steps]))
             line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": world, "steps": a.steps,
                     "warmup": a.warmup, "ms_per_step": a.batch / v * 1e3, "higher_is_better": True,
                     "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
                     "impl": "reference",
-                    "cpu_baseline": {**steps[-1], "value": v},
+                    "cpu_baseline": {**steps[-1], "value": v,
+                                     "step_spread": spread(s["value"] for s in steps)},
                     "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
             print(json.dumps(line), flush=True)
         if dist:
@@ -669,7 +946,9 @@ def main() -> None:
         return
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        cpu = cpu_baseline(a.ctx, 128, a.m, a.n, G, units_per_step, a.batch, a.cpu_seconds)
+        cb = CpuBaseline(a.ctx, 128, a.m, a.n, G, units_per_step, a.batch)
+        cpu = cb.sample(a.cpu_seconds)
+        cb.close()
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -682,16 +961,24 @@ def main() -> None:
             "higher_is_better": True,
             "scaling": "strong" if heads else "weak",
             "vs_baseline": None,
-            "dtype": "f32",
-            "data": "synthetic (on-device Philox: lognormal radii, uniform angles, 2 outlier channels)",
+            "dtype": "bf16",
+            "dtype_detail": (f"q, out and {a.values} values as stored; {a.m}-bit angle / {a.n}-bit radius key "
+                             "codes; scores via fp16 hi+lo tensor-core products with fp32 accumulation; "
+                             "online softmax and P.V accumulation in fp32"),
+            "data": "synthetic (on-device Philox: lognormal radii, uniform angles, 2 outlier channels; "
+                    "N(0,1) values and queries)",
             "config": config,
+            "value_reps": res["value_reps"],
             "roofline": res["roofline"],
             "cpu_baseline": cpu,
             "e2e": {"value": res["e2e_value"], "unit": "tokens/s", "ms_per_step": res["e2e_ms"],
-                    "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"]},
+                    "h2d_bytes_per_step": res["h2d"], "d2h_bytes_per_step": res["d2h"], "reps": res["e2e_reps"],
+                    "path": "public API per layer (UnitView.decode / decode_peer + wait) with pinned host q in "
+                            "and outputs out every step, copies overlapped on copy streams"},
             "clocks": res["clocks"],
             "sustained": res.get("sustained"),
             "gpu_launches": res["gpu_launches"],
+            "parity": res.get("parity"),
             "extras": res.get("extras"),
         }
         print(json.dumps(line), flush=True)

@@ -105,7 +105,8 @@ def attention_weights(scores, temperature: float) -> np.ndarray:
     if s.numel() == 0:
         raise ValueError("cannot take attention weights of an empty score vector")
     out = torch.empty(s.numel(), dtype=torch.float64, device=dev)
-    _lib.call("pqb_softmax_f64", ptr(s.contiguous()), s.numel(), float(temperature), ptr(out), stream_ptr(dev))
+    s = s.contiguous()
+    _lib.call("pqb_softmax_f64", ptr(s), s.numel(), float(temperature), ptr(out), stream_ptr(dev))
     return out.cpu().numpy()
 
 

@@ -319,7 +319,7 @@ class PolarKVCache:
             r = torch.frombuffer(bytearray(codes.radius_stream), dtype=torch.uint8).to(dev)
             _lib.call("pqb_import_streams", self.store_ref(), unit, self.dim, cfg.angle_bits, cfg.radius_bits, Tq,
                       ptr(a), ptr(r), stream_ptr(dev))
-        self.scales16[unit] = torch.from_numpy(np.ascontiguousarray(scales.values, dtype=np.float16)).to(dev)
+        self.scales16[unit] = torch.from_numpy(np.array(scales.values, dtype=np.float16)).to(dev)
         flags = new_flags(dev)
         if res.shape[0]:
             kr = torch.from_numpy(res).to(dev).unsqueeze(0)

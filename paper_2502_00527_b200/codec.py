@@ -63,9 +63,10 @@ def encode_device(keys: torch.Tensor, scales: torch.Tensor, cfg: QuantConfig, st
     U, T, d = k3.shape
     dev = k3.device
     flags = flags if flags is not None else new_flags(dev)
+    sc = scales.contiguous()
     _lib.call(
         "pqb_encode", ptr(k3), dtype_code(k3), U, T, d, k3.stride(0), k3.stride(1), layout_code(cfg.layout),
-        cfg.angle_bits, cfg.radius_bits, ptr(scales.contiguous()), store_ref, ptr(tok_offset), tok_offset_const,
+        cfg.angle_bits, cfg.radius_bits, ptr(sc), store_ref, ptr(tok_offset), tok_offset_const,
         ptr(clamp_counts), ptr(flags), stream_ptr(dev),
     )
 
@@ -253,7 +254,8 @@ def quantize_angle(theta, angle_bits: int) -> np.ndarray:
     n = th.size
     out = torch.empty(n, dtype=torch.uint8, device=dev)
     if n:
-        _lib.call("pqb_quantize_angle", ptr(_to_device(th.reshape(-1), dev)),
+        thd = _to_device(th.reshape(-1), dev)  # held until the call is enqueued
+        _lib.call("pqb_quantize_angle", ptr(thd),
                   _lib.PQB_F32 if dt == np.float32 else _lib.PQB_F64, n, angle_bits, ptr(out), stream_ptr(dev))
     return _scalar_or_array(out.cpu().numpy().reshape(th.shape), th.ndim)
 
@@ -280,8 +282,9 @@ def quantize_radius_counted(radius, scale, radius_bits: int) -> tuple[np.ndarray
     out = torch.empty(n, dtype=torch.uint8, device=dev)
     clamped = torch.zeros(1, dtype=torch.int64, device=dev)
     if n:
-        _lib.call("pqb_quantize_radius", ptr(_to_device(rb.reshape(-1), dev)),
-                  _lib.PQB_F32 if dt == np.float32 else _lib.PQB_F64, ptr(_to_device(sb.reshape(-1), dev)), n,
+        rd, sd = _to_device(rb.reshape(-1), dev), _to_device(sb.reshape(-1), dev)  # both alive across the call
+        _lib.call("pqb_quantize_radius", ptr(rd),
+                  _lib.PQB_F32 if dt == np.float32 else _lib.PQB_F64, ptr(sd), n,
                   radius_bits, ptr(out), ptr(clamped), stream_ptr(dev))
     return _scalar_or_array(out.cpu().numpy().reshape(rb.shape), rb.ndim), int(clamped.item())
 
