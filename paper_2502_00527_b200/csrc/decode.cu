@@ -738,7 +738,8 @@ static int dispatch_fast(const DecodeArgs& a, cudaStream_t s, bool& handled) {
 int launch_decode(const DecodeArgs& a, cudaStream_t s) {
   const pqb_cache& c = *a.cache;
   const bool vq = c.store.value_dtype == PQB_VQ4 && a.out != nullptr;  // 4-bit values: DQ kernel or generic
-  const bool fast_ok = c.d == 128 && (a.out == nullptr || c.store.value_dtype == PQB_BF16 || vq) &&
+  const bool f32v = c.store.value_dtype == PQB_F32 && a.out != nullptr;  // fp32 values: DQ kernel or generic
+  const bool fast_ok = c.d == 128 && (a.out == nullptr || c.store.value_dtype == PQB_BF16 || vq || f32v) &&
                        (a.group == 1 || a.group == 4 || a.group == 8) && c.store.page_tokens % kTile == 0 &&
                        (c.store.angle_off % 16 == 0) && (c.store.radius_off % 16 == 0) &&
                        (c.store.value_off % 16 == 0 || a.out == nullptr) && (c.store.page_bytes % 16 == 0) &&
@@ -752,7 +753,7 @@ int launch_decode(const DecodeArgs& a, cudaStream_t s) {
     set_error("peer-gather decode needs the DQ kernel (group 4 or 8, d = 128, a fast-path store and bit widths)");
     return PQB_EUNSUPPORTED;
   }
-  if (fast_ok && !handled && !vq && !(a.flags & PQB_DECODE_FORCE_GENERIC)) {
+  if (fast_ok && !handled && !vq && !f32v && !(a.flags & PQB_DECODE_FORCE_GENERIC)) {
     // scores requested -> the bit-exact scoring sequence; fused-only -> FMA form
     const int rc = a.scores != nullptr ? dispatch_fast<true>(a, s, handled) : dispatch_fast<false>(a, s, handled);
     if (rc != PQB_OK) return rc;

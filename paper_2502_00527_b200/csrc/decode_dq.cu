@@ -85,18 +85,27 @@ constexpr int kDqThreads = kDqWs ? (kNW + 4) * 32 : kNW * 32;
 constexpr int kConsThreads = kNW * 32;
 static_assert(!kDqWs || kNW == 8, "producer j serves compute warps j and j + 4");
 
+// Value-cache treatments (template parameter VQ): the page's value region as
+// the decode kernel streams it.
+constexpr int kValBf16 = 0;  // bf16 rows, tensor-core P.V (hi/lo P)
+constexpr int kValVq4 = 1;   // PQB_VQ4: 4-bit per-token codes + (zp, scale), tensor-core P.V
+constexpr int kValF32 = 2;   // PQB_F32: the reference's default fp32 rows (kv_cache.py:8-9, :209), CUDA-core P.V
+
 template <int G, int M, int N, int VQ = 0>
 struct DqCfg {
   static constexpr int kABytes = kTile * 8 * M;
   static constexpr int kRBytes = kTile * 8 * N;
-  // bf16 value rows, or (VQ) 2 KB of fragment-order 4-bit codes + 32 (zp, scale)
-  static constexpr int kVBytes = VQ ? 2048 + kTile * 8 : kTile * 256;
+  // bf16 value rows, 2 KB of fragment-order 4-bit codes + 32 (zp, scale), or fp32 rows
+  static constexpr int kVBytes = VQ == kValVq4 ? 2048 + kTile * 8 : VQ == kValF32 ? kTile * 512 : kTile * 256;
   static constexpr int kStageBytes = kABytes + kRBytes + kVBytes;
+  // stages per compute warp: fp32 rows make an 18 KB stage, so one per warp
+  // (8 in flight per SM, double the bytes of the bf16 ring's 16 x 10 KB)
+  static constexpr int kSt = VQ == kValF32 ? 1 : kStages;
   static constexpr int kPBytes = kTile * 8 * 4;              // fp32 [32 tokens][8 queries] residual-dot scratch
   static constexpr int kTabBytes = 128 << (M + N);          // product table, 16 bank-slot copies
   static constexpr int kFragBytes = 16 * 32 * 16;            // Q' A-fragments [ks][lane] uint4 (hi, lo, hi, lo)
   static constexpr int kHeadBytes = kTabBytes + kFragBytes + G * 128 * 4 + 128 + 8 * (1 << M);
-  static constexpr int kWarpBytes = kStages * kStageBytes + kPBytes;
+  static constexpr int kWarpBytes = kSt * kStageBytes + kPBytes;
 #if PQB_DQ_PRMT_TAB
   // the whole opt-in budget minus the 256 B of static barriers; the kernel
   // checks that its stages fit around the table
@@ -106,7 +115,7 @@ struct DqCfg {
 #endif
   static constexpr bool kPacked = G <= 4;  // P.V: columns 0-3 carry P_hi, 4-7 P_lo
   static_assert(kHeadBytes % 16 == 0 && kWarpBytes % 16 == 0, "alignment");
-  static_assert(kNW * kStages * kStageBytes >= kNW * G * 132 * 4, "merge area");
+  static_assert(kNW * kSt * kStageBytes >= kNW * G * 132 * 4, "merge area");
 };
 
 PQB_DEV uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
@@ -277,12 +286,12 @@ PQB_DEV void issue_tile_dq(uint8_t* st, const pqb_store& s, const uint8_t* pb, i
     mbar_arrive_expect_tx(bar, kA + kR);
     bulk_g2s(st, pb + s.angle_off + in_page * 8 * M, kA, bar);
     bulk_g2s(st + kA, pb + s.radius_off + in_page * 8 * N, kR, bar);
-  } else if constexpr (!VQ) {
-    constexpr uint32_t kV = kTile * 256;
+  } else if constexpr (VQ == kValBf16 || VQ == kValF32) {
+    constexpr uint32_t kRow = VQ == kValF32 ? 512 : 256, kV = kTile * kRow;
     mbar_arrive_expect_tx(bar, kA + kR + kV);
     bulk_g2s(st, pb + s.angle_off + in_page * 8 * M, kA, bar);
     bulk_g2s(st + kA, pb + s.radius_off + in_page * 8 * N, kR, bar);
-    bulk_g2s(st + kA + kR, pb + s.value_off + in_page * 256, kV, bar);
+    bulk_g2s(st + kA + kR, pb + s.value_off + static_cast<int64_t>(in_page) * kRow, kV, bar);
   } else {
     mbar_arrive_expect_tx(bar, kA + kR + 2048 + kTile * 8);
     bulk_g2s(st, pb + s.angle_off + in_page * 8 * M, kA, bar);
@@ -317,6 +326,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     decode_dq_kernel(const pqb_cache c, const void* __restrict__ q, int q_dtype, float sm_scale_log2, EpiArgs ep,
                      WorkSplit ws, float* __restrict__ scores, int64_t scores_ld) {
   using Cfg = DqCfg<G, M, N, VQ>;
+  constexpr int kSt = Cfg::kSt;
+  constexpr bool kVq4 = VQ == kValVq4, kVf32 = VQ == kValF32;
   constexpr bool kScores = PROBE == kDqScores;
   constexpr bool kFused = M == 4 && N == 4;
   constexpr bool kPacked = Cfg::kPacked;
@@ -338,7 +349,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   };
   uint8_t* warp_area = smem;  // merge scratch aliases the first stages (all before the table)
   if (tid == 0 && (tab_off < 0 || n_before * Cfg::kStageBytes < kNW * G * 132 * 4 ||
-                   tab_off + 65536 + (kNW * kStages - n_before) * Cfg::kStageBytes > Cfg::kSmem))
+                   tab_off + 65536 + (kNW * kSt - n_before) * Cfg::kStageBytes > Cfg::kSmem))
     __trap();  // shared-window layout other than measured: the table cannot sit at kPtTabAbs
   const GapArr<float> rbuf{tabp, kGapRbuf + 8 * (warp < kNW ? warp : 0)};
 #else
@@ -349,10 +360,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   float2* cs_s = reinterpret_cast<float2*>(reinterpret_cast<uint8_t*>(s_misc) + 128);  // [2^M] (cos, sin)
   uint8_t* warp_area = smem + Cfg::kHeadBytes;
   auto stage_ptr = [&](int i) -> uint8_t* {
-    return warp_area + (i / kStages) * Cfg::kWarpBytes + (i % kStages) * Cfg::kStageBytes;
+    return warp_area + (i / kSt) * Cfg::kWarpBytes + (i % kSt) * Cfg::kStageBytes;
   };
   float* rbuf = reinterpret_cast<float*>(warp_area + (warp < kNW ? warp : 0) * Cfg::kWarpBytes +
-                                         kStages * Cfg::kStageBytes);  // [32][8]
+                                         kSt * Cfg::kStageBytes);  // [32][8]
 #endif
   // mbarriers live outside the warp areas: the end-of-segment merge scratch
   // (red, G * 132 floats per warp) aliases the stage memory and, at G = 8,
@@ -431,11 +442,11 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           c0.init(t_lo + w0, tpp);
           c1.init(t_lo + w1, tpp);
           auto issue = [&](int w, uint32_t it, const TileCursor& cu) {
-            const uint32_t s = it % kStages;
-            // the ring starts empty: the first kStages fills need no release
-            if (it >= kStages) mbar_wait(&s_empty[w][s], ((it / kStages) & 1) ^ 1);
+            const uint32_t s = it % kSt;
+            // the ring starts empty: the first kSt fills need no release
+            if (it >= kSt) mbar_wait(&s_empty[w][s], ((it / kSt) & 1) ^ 1);
             fence_proxy_async_smem();
-            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(w * kStages + s), c.store,
+            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(w * kSt + s), c.store,
                                     page_base_c(c.store, unit, PROBE == 2 ? 0 : cu.pg), PROBE == 2 ? 0 : cu.tin,
                                     &s_bar[w][s]);
           };
@@ -540,11 +551,11 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     cur.init(first, tpp);
     if (!kDqWs && lane == 0) {
 #pragma unroll
-      for (int s = 0; s < kStages; ++s) {
+      for (int s = 0; s < kSt; ++s) {
         if (cur.tile < t_hi) {
           fence_proxy_async_smem();
-          const uint32_t sl = (k_iter + s) % kStages;
-          issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kStages + sl), c.store,
+          const uint32_t sl = (k_iter + s) % kSt;
+          issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kSt + sl), c.store,
                                   page_base_c(c.store, unit, PROBE == 2 ? 0 : cur.pg), PROBE == 2 ? 0 : cur.tin,
                                   bar + sl);
         }
@@ -559,12 +570,17 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
       for (int k = 0; k < 4; ++k) d[mt][k] = 0.0f;
+    float o[G][4];  // fp32 values: output dims 4 lane .. 4 lane + 3 of every query
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[g][k] = 0.0f;
 
     for (int tile = first; tile < t_hi; tile += kNW, ++k_iter) {
-      const uint32_t s = k_iter % kStages;
-      const int nt = tile + kStages * kNW;  // the tile this stage is refilled with
-      mbar_wait(bar + s, (k_iter / kStages) & 1);
-      const uint8_t* st = stage_ptr(warp * kStages + s);
+      const uint32_t s = k_iter % kSt;
+      const int nt = tile + kSt * kNW;  // the tile this stage is refilled with
+      mbar_wait(bar + s, (k_iter / kSt) & 1);
+      const uint8_t* st = stage_ptr(warp * kSt + s);
       const int tok0 = tile * kTile;
       if constexpr (PROBE == 1) {
         __syncwarp();
@@ -573,7 +589,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         } else if (lane == 0) {
           if (nt < t_hi) {
             fence_proxy_async_smem();
-            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kStages + s), c.store, page_base_c(c.store, unit, cur.pg), cur.tin,
+            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kSt + s), c.store, page_base_c(c.store, unit, cur.pg), cur.tin,
                                     bar + s);
           }
           cur.next(dpg, dtin, tpp);
@@ -596,7 +612,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         }
         // m = n = 4 with bf16 values: two chains per n-block (A/B +1% G = 4, +3% G = 8);
         // the other instances measured better with one (m3n2 -6%, 4-bit values -1.5%)
-        constexpr bool kTwoChains = kFused && !VQ;
+        constexpr bool kTwoChains = kFused && !kVq4;
 #pragma unroll
         for (int ks = 0; ks < 16; ks += 2) {
 #pragma unroll
@@ -673,7 +689,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         } else if (lane == 0) {
           if (nt < t_hi) {
             fence_proxy_async_smem();
-            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kStages + s), c.store, page_base_c(c.store, unit, cur.pg),
+            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kSt + s), c.store, page_base_c(c.store, unit, cur.pg),
                                              cur.tin, bar + s);
           }
           cur.next(dpg, dtin, tpp);
@@ -695,13 +711,57 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       const float alpha = fast_exp2(m_run - mn);
       const bool rescale = mn != m_run;
       m_run = mn;
+      if constexpr (kVf32) {
+        // ---- fp32 values (the reference's default cache): P.V on the CUDA
+        // cores in full fp32.  P goes through the warp's [32 tokens][8] buffer;
+        // lane L owns output dims 4L .. 4L + 3 and reads each fp32 value row
+        // with one conflict-free LDS.128 (512 B per row = 4 wavefronts) and the
+        // row's G probabilities as broadcast LDS.128s.
+        float ls = 0.0f;
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+          const float p0 = fast_exp2(x[nb][0] - mn), p1 = fast_exp2(x[nb][1] - mn);
+          ls += p0 + p1;
+          if (g8 < G) {
+            rbuf[(8 * nb + 2 * t4) * 8 + g8] = p0;
+            rbuf[(8 * nb + 2 * t4 + 1) * 8 + g8] = p1;
+          }
+        }
+        l_run = fmaf(l_run, alpha, ls);
+        if (__any_sync(0xffffffffu, rescale && g8 < G)) {
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float ag = __shfl_sync(0xffffffffu, alpha, g * 4);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) o[g][k] *= ag;
+          }
+        }
+        __syncwarp();
+        const float4* vrow = reinterpret_cast<const float4*>(st + Cfg::kABytes + Cfg::kRBytes) + lane;
+#pragma unroll 8
+        for (int t = 0; t < kTile; ++t) {
+          const float4 v = vrow[t * 32];
+#pragma unroll
+          for (int g4 = 0; g4 < G; g4 += 4) {
+            const float4 pv = *reinterpret_cast<const float4*>(&rbuf[t * 8 + g4]);
+            const float pg[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+            for (int k = 0; k < 4 && g4 + k < G; ++k) {
+              o[g4 + k][0] = fmaf(pg[k], v.x, o[g4 + k][0]);
+              o[g4 + k][1] = fmaf(pg[k], v.y, o[g4 + k][1]);
+              o[g4 + k][2] = fmaf(pg[k], v.z, o[g4 + k][2]);
+              o[g4 + k][3] = fmaf(pg[k], v.w, o[g4 + k][3]);
+            }
+          }
+        }
+      } else {
       float ls = 0.0f, zs = 0.0f, bs = 0.0f;
       uint32_t phi[4], plo[4];  // bf16x2 (tokens 8 nb + 2 t4, +1)
 #pragma unroll
       for (int nb = 0; nb < 4; ++nb) {
         float p0 = fast_exp2(x[nb][0] - mn), p1 = fast_exp2(x[nb][1] - mn);
         ls += p0 + p1;
-        if constexpr (VQ) {  // (zp, scale) of tokens 8 nb + 2 t4, +1
+        if constexpr (kVq4) {  // (zp, scale) of tokens 8 nb + 2 t4, +1
           const float4 zsv =
               reinterpret_cast<const float4*>(st + Cfg::kABytes + Cfg::kRBytes + 2048)[4 * nb + t4];
           zs = fmaf(p0, zsv.x, fmaf(p1, zsv.z, zs));
@@ -713,13 +773,13 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
         phi[nb] = *reinterpret_cast<const uint32_t*>(&hi);
         plo[nb] = *reinterpret_cast<const uint32_t*>(&lo);
-        if constexpr (VQ) {
+        if constexpr (kVq4) {
           const float2 lf = __bfloat1622float2(lo);
           bs += (hf.x + hf.y) + (lf.x + lf.y);
         }
       }
       l_run = fmaf(l_run, alpha, ls);
-      if constexpr (VQ) {
+      if constexpr (kVq4) {
         z_run = fmaf(z_run, alpha, zs);
         b_run = fmaf(b_run, alpha, bs);
       }
@@ -742,7 +802,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       }
       // ---- P.V on tensor cores: O^T[128 x 8] += V^T[128 x 32] . P^T[32 x 8];
       // the P^T B-fragments are the score registers (k-step ks = n-blocks 2ks, 2ks+1)
-      if constexpr (VQ) {
+      if constexpr (kVq4) {
         // A fragments straight from the code words: nibble -> bf16 (128 + c) by
         // OR-ing into the bit pattern of 128.0; the 128 * sum(B) it adds is
         // removed per query in the epilogue, with sum(B) taken over the exact
@@ -774,13 +834,14 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           }
         }
       }
+      }  // bf16 / 4-bit values
       __syncwarp();
       if (kDqWs) {
         if (lane == 0) mbar_arrive(&s_empty[warp][s]);
       } else if (lane == 0) {
         if (nt < t_hi) {
           fence_proxy_async_smem();
-          issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kStages + s), c.store,
+          issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kSt + s), c.store,
                                   page_base_c(c.store, unit, PROBE == 2 ? 0 : cur.pg), PROBE == 2 ? 0 : cur.tin,
                                   bar + s);
         }
@@ -795,13 +856,13 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     // ---- segment epilogue: per-warp (m, l, o) -> shared, then the common merge
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
-    if constexpr (kPacked) {  // O = columns q (P_hi) + q + 4 (P_lo): lanes t4, t4 ^ 2
+    if constexpr (kPacked && !kVf32) {  // O = columns q (P_hi) + q + 4 (P_lo): lanes t4, t4 ^ 2
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt)
 #pragma unroll
         for (int k = 0; k < 4; ++k) d[mt][k] += __shfl_xor_sync(0xffffffffu, d[mt][k], 2);
     }
-    if constexpr (VQ) {  // + sum_t p_t zp_t - 128 sum_t B_t of the column's query
+    if constexpr (kVq4) {  // + sum_t p_t zp_t - 128 sum_t B_t of the column's query
       z_run += __shfl_xor_sync(0xffffffffu, z_run, 1);
       z_run += __shfl_xor_sync(0xffffffffu, z_run, 2);
       b_run += __shfl_xor_sync(0xffffffffu, b_run, 1);
@@ -823,7 +884,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       mine[g8 * 132] = m_run;
       mine[g8 * 132 + 1] = l_run;
     }
-    if (qc0 < G && (!kPacked || t4 < 2)) {
+    if constexpr (kVf32) {
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mine[g * 132 + 4 + 4 * lane + k] = o[g][k];
+    } else if (qc0 < G && (!kPacked || t4 < 2)) {
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
         const int dim = 16 * mt + g8;
@@ -864,7 +930,7 @@ static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws
       const int tab_off = static_cast<int>(kPtTabAbs) - dyn0;
       const int n_before = tab_off / Cfg::kStageBytes;
       if (tab_off < 0 || n_before * Cfg::kStageBytes < kNW * G * 132 * 4 ||
-          tab_off + 65536 + (kNW * kStages - n_before) * Cfg::kStageBytes > Cfg::kSmem ||
+          tab_off + 65536 + (kNW * Cfg::kSt - n_before) * Cfg::kStageBytes > Cfg::kSmem ||
           stat + Cfg::kSmem > 232448)
         return kDqLayoutUnavailable;  // the caller falls back to the linear-layout build
     }
@@ -913,12 +979,23 @@ static int dispatch_dq_mn(const DecodeArgs& a, const EpiArgs& ep, const WorkSpli
   }
   if (a.cache->store.value_dtype == PQB_VQ4) {
     switch (mn) {
-      case 44: return launch_dq<G, 4, 4, 0, 1>(a, ep, ws, grid, s);
-      case 32: return launch_dq<G, 3, 2, 0, 1>(a, ep, ws, grid, s);
-      case 22: return launch_dq<G, 2, 2, 0, 1>(a, ep, ws, grid, s);
-      case 42: return launch_dq<G, 4, 2, 0, 1>(a, ep, ws, grid, s);
-      case 24: return launch_dq<G, 2, 4, 0, 1>(a, ep, ws, grid, s);
-      case 34: return launch_dq<G, 3, 4, 0, 1>(a, ep, ws, grid, s);
+      case 44: return launch_dq<G, 4, 4, 0, kValVq4>(a, ep, ws, grid, s);
+      case 32: return launch_dq<G, 3, 2, 0, kValVq4>(a, ep, ws, grid, s);
+      case 22: return launch_dq<G, 2, 2, 0, kValVq4>(a, ep, ws, grid, s);
+      case 42: return launch_dq<G, 4, 2, 0, kValVq4>(a, ep, ws, grid, s);
+      case 24: return launch_dq<G, 2, 4, 0, kValVq4>(a, ep, ws, grid, s);
+      case 34: return launch_dq<G, 3, 4, 0, kValVq4>(a, ep, ws, grid, s);
+      default: handled = false; return PQB_OK;
+    }
+  }
+  if (a.cache->store.value_dtype == PQB_F32) {
+    switch (mn) {
+      case 44: return launch_dq<G, 4, 4, 0, kValF32>(a, ep, ws, grid, s);
+      case 32: return launch_dq<G, 3, 2, 0, kValF32>(a, ep, ws, grid, s);
+      case 22: return launch_dq<G, 2, 2, 0, kValF32>(a, ep, ws, grid, s);
+      case 42: return launch_dq<G, 4, 2, 0, kValF32>(a, ep, ws, grid, s);
+      case 24: return launch_dq<G, 2, 4, 0, kValF32>(a, ep, ws, grid, s);
+      case 34: return launch_dq<G, 3, 4, 0, kValF32>(a, ep, ws, grid, s);
       default: handled = false; return PQB_OK;
     }
   }

@@ -513,3 +513,38 @@ def test_decode_launch_count_policy():
     assert lib.pqb_decode_launches(128, 4, 32768, pq._lib.PQB_DECODE_MERGE_KERNEL) == 2
     assert lib.pqb_decode_launches(8, 4, 4096, pq._lib.PQB_DECODE_NO_COMBINE) == 1
     assert lib.pqb_decode_launches(8, 1, 4096, 0) == 1  # LUT kernel: merge in-kernel
+
+
+@pytest.mark.parametrize("m,n", [(4, 4), (3, 2), (2, 4), (3, 4)])
+@pytest.mark.parametrize("G", [4, 8])
+@pytest.mark.parametrize("lay,res,page", [(1, 0, 256), (0, 40, 64), (1, 16, 32)])
+def test_f32_values_dq_vs_oracle(m, n, G, lay, res, page):
+    """The reference's default value cache (fp32 rows, kv_cache.py:8-9, :209)
+    in the DQ kernel (one 18 KB stage per warp, fp32 P.V on the CUDA cores):
+    fp32 output within 1e-4 of softmax64(LUT scores) . V with the exact fp32
+    values; the linear-layout build and the generic kernel agree."""
+    lens = [3000, 1777, 33]
+    U, T = len(lens), max(lens)
+    keys = [po.synthetic_keys(t, 128, seed=300 + u, outliers=(0, 1), layout=lay) for u, t in enumerate(lens)]
+    rng = np.random.default_rng(m * 100 + n * 10 + G)
+    vals = [rng.standard_normal((t, 128)).astype(np.float32) * 3 for t in lens]
+    q = rng.standard_normal((U, G, 128)).astype(np.float32)
+    cache = pq.PolarKVCache(pq.QuantConfig(m, n, LAY[lay]), U, 128, res, capacity=T + 1, page_tokens=page,
+                            value_dtype=torch.float32, shuffle_pages=True)
+    for u in range(U):
+        cache.prefill(torch.from_numpy(keys[u]).cuda().unsqueeze(0), torch.from_numpy(vals[u]).cuda().unsqueeze(0),
+                      unit_start=u)
+    qd = torch.from_numpy(q).cuda()
+    outs = [cache.decode(qd).cpu().numpy(),
+            cache._all().decode(qd, flags=pq._lib.PQB_DECODE_DQ | pq._lib.PQB_DECODE_DQ_LINEAR).cpu().numpy(),
+            cache._all().decode(qd, flags=pq._lib.PQB_DECODE_FORCE_GENERIC).cpu().numpy()]
+    for u in range(U):
+        a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
+        s16 = cache.scales16[u].cpu().numpy()
+        resid = keys[u][lens[u] - min(res, lens[u]):] if res else np.zeros((0, 128), np.float32)
+        v64 = vals[u].astype(np.float64)
+        for g in range(G):
+            ref = po.lut_scores(q[u, g], a, r, s16, m, n, lay, resid)
+            o_ref = po.softmax64(ref, 1.0 / math.sqrt(128)) @ v64
+            for o in outs:
+                peak_close(o[u, g], o_ref, OUT_RTOL_F32)
