@@ -85,7 +85,7 @@ def parse():
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no timing claims)")
     ap.add_argument("--variant", choices=["auto", "lut", "dq"], default="auto",
                     help="scoring kernel of the fused decode (auto: the library's per-G choice)")
-    ap.add_argument("--values", choices=["bf16", "f32", "vq4"], default="bf16",
+    ap.add_argument("--values", choices=["bf16", "f32", "vq2", "vq4", "vq8"], default="bf16",
                     help="value-cache treatment of the headline workload")
     return ap.parse_args()
 
@@ -165,9 +165,10 @@ class ClockSampler:
 def unit_bytes(T: int, G: int, d: int, m: int, n: int, values: str = "bf16") -> int:
     """Algorithmic HBM bytes of one (sequence, layer, kv-head) unit per decode
     step: codes once per KV head, V once (bf16 rows, fp32 rows,
-    or 4-bit codes + fp32 (zp, scale) per token), fp16 scales, bf16 q in /
+    or b-bit codes + fp32 (zp, scale) per token), fp16 scales, bf16 q in /
     bf16 out for the G query heads."""
-    v = {"bf16": T * d * 2, "f32": T * d * 4, "vq4": T * (d // 2 + 8)}[values]
+    v = {"bf16": T * d * 2, "f32": T * d * 4, "vq2": T * (d // 4 + 8), "vq4": T * (d // 2 + 8),
+         "vq8": T * (d + 8)}[values]
     return T * (d // 2) * (m + n) // 8 + v + (d // 2) * 2 + 2 * G * d * 2
 
 
@@ -307,7 +308,7 @@ class DecodeWorkload:
         cfg = pq.QuantConfig(m, n)
         self.cache = pq.PolarKVCache(cfg, layers * self.upl, 128, 0, capacity=T, page_tokens=page_tokens,
                                      value_dtype=torch.float32 if values == "f32" else torch.bfloat16, device=dev,
-                                     value_bits=4 if values == "vq4" else None)
+                                     value_bits=int(values[2:]) if values.startswith("vq") else None)
         syn = pq.SyntheticConfig(T, 128, outlier_channels=frozenset({0, 1}))
         chunk = max(1, min(self.upl, (1 << 31) // (T * 128 * 2)))  # <= 2 GB bf16 staging per tensor
         keep = set(int(u) for u in keep)
@@ -476,7 +477,7 @@ class DecodeWorkload:
             a, r = self.cache.code_arrays(u)
             # 4-bit values: the reference's dequantized rows (values(), bit-identical to
             # quantize_uniform / dequantize_uniform, tests/test_oracle_golden.py)
-            v = self.cache.values_f32(u) if self.values == "vq4" else vals.float()
+            v = self.cache.values_f32(u) if self.values.startswith("vq") else vals.float()
             jobs.append(dict(keys=keys.float().cpu().numpy(), s16_gpu=self.cache.scales16[u].cpu().numpy(),
                              angle_gpu=a.cpu().numpy(), radius_gpu=r.cpu().numpy(), m=self.m, n=self.n,
                              q=self.q[layer, j].float().cpu().numpy(), values=v.cpu().numpy(),
@@ -684,11 +685,14 @@ def run_extras(dev, a, rank: int, world: int, dist) -> dict:
             # configs[1] with the reference's value-quantization mode
             # (PackedKVCache(quantize_values=True, value_bits=4)) read inside the kernel
             "configs[1]_vq4_values": dict(layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, values="vq4"),
+            "configs[1]_vq2_values": dict(layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, values="vq2"),
+            "configs[1]_vq8_values": dict(layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, values="vq8"),
             # the reference's default value cache: full-precision fp32 rows (kv_cache.py:8-9, :209)
             "configs[1]_f32_values": dict(layers=32, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, values="f32"),
         }
         parity_of = {"configs[2]_P1_L32_B8_128K_m3n2", "configs[3]_per_gpu_L80_B32_32K_G8_1kvhead",
-                     "configs[1]_f32_values", "configs[1]_vq4_values"}
+                     "configs[1]_f32_values", "configs[1]_vq4_values", "configs[1]_vq2_values",
+                     "configs[1]_vq8_values"}
         for name, s in specs.items():
             try:
                 upl = s["batch"] * s["hkv"]

@@ -68,6 +68,10 @@ extern "C" {
  * MMA-fragment order, see INTEGRATION.md] then [page_tokens][zp, scale] fp32.
  * Read back: fl(fl(code * scale) + zp) (dequantize_uniform, :143-167). */
 #define PQB_VQ4 16
+/* The same with 2-bit and 8-bit codes (value_bits 2 / 8): a tile's codes take
+ * 512 * bits bytes, then [page_tokens][zp, scale]. */
+#define PQB_VQ2 17
+#define PQB_VQ8 18
 
 /* pairing layouts: same numeric values as PairingLayout (tensor_core.py:41-50) */
 #define PQB_ADJACENT 0
@@ -91,7 +95,7 @@ typedef struct pqb_store {
   const int32_t* page_table;
   int32_t max_pages;
   int32_t page_tokens;
-  int32_t value_dtype; /* PQB_F32, PQB_BF16 or PQB_VQ4 */
+  int32_t value_dtype; /* PQB_F32, PQB_BF16, PQB_VQ2, PQB_VQ4 or PQB_VQ8 */
   int32_t reserved;
 } pqb_store;
 

@@ -19,6 +19,7 @@ PQB_FLAG_NONFINITE, PQB_FLAG_SCALE_OVERFLOW = 1, 2
 PQB_F32, PQB_BF16, PQB_F16 = 0, 1, 2
 PQB_F64 = 3  # element-wise reference API only
 PQB_VQ4 = 16  # pqb_store.value_dtype: 4-bit per-token value codes
+PQB_VQ2, PQB_VQ8 = 17, 18  # 2- / 8-bit per-token value codes
 PQB_DECODE_FORCE_GENERIC, PQB_DECODE_NO_COMBINE, PQB_DECODE_DQ, PQB_DECODE_LUT = 1, 2, 4, 8
 PQB_DECODE_PROBE_MEM, PQB_DECODE_PROBE_COMPUTE = 64, 128
 PQB_DECODE_MERGE_KERNEL = 256

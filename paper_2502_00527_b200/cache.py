@@ -49,6 +49,7 @@ from .core import (
 )
 
 SCALE_BITS = 16  # kv_cache.py:39
+VQ_DTYPE = {2: _lib.PQB_VQ2, 4: _lib.PQB_VQ4, 8: _lib.PQB_VQ8}  # value_bits -> paged code layout
 RESIDUAL_BITS = 16  # kv_cache.py:40
 
 
@@ -82,9 +83,10 @@ class PolarKVCache:
             # per-token uniform value codes (PackedKVCache(quantize_values=True), kv_cache.py:199-209)
             if not 1 <= int(value_bits) <= 8:
                 raise ValueError(f"bits must be in [1, 8], got {value_bits}")
-            if int(value_bits) != 4 or dim != 128:
-                raise ValueError("the batched cache stores quantized values as 4-bit codes with dim = 128 "
-                                 f"(got value_bits={value_bits}, dim={dim})")
+            if int(value_bits) not in VQ_DTYPE or dim != 128:
+                raise ValueError("the batched cache stores quantized values as 2-, 4- or 8-bit codes with dim = 128 "
+                                 f"(got value_bits={value_bits}, dim={dim}); PackedKVCache keeps other widths "
+                                 "as their dequantized fp32 rows")
         self.device = require_cuda(device)
         self.cfg = cfg
         self.n_units = int(n_units)
@@ -100,7 +102,7 @@ class PolarKVCache:
         a_bytes = P * half * cfg.angle_bits // 8
         r_bytes = P * half * cfg.radius_bits // 8
         if self.value_bits is not None:
-            v_bytes = P * 64 + P * 8  # 4-bit codes (MMA-fragment order) + (zp, scale) fp32 per token
+            v_bytes = P * 16 * self.value_bits + P * 8  # b-bit codes (MMA-fragment order) + (zp, scale) fp32 per token
         else:
             v_bytes = P * dim * (4 if value_dtype == torch.float32 else 2)
         self.angle_off = 0
@@ -156,7 +158,7 @@ class PolarKVCache:
             page_table=ptr(self.page_table),
             max_pages=self.max_pages,
             page_tokens=self.page_tokens,
-            value_dtype=(_lib.PQB_VQ4 if self.value_bits is not None
+            value_dtype=(VQ_DTYPE[self.value_bits] if self.value_bits is not None
                          else _lib.PQB_F32 if self.value_dtype == torch.float32 else _lib.PQB_BF16),
             reserved=0,
         )
@@ -211,7 +213,7 @@ class PolarKVCache:
     def bytes_per_token(self) -> int:
         half = self.dim // 2
         if self.value_bits is not None:
-            return half * (self.cfg.angle_bits + self.cfg.radius_bits) // 8 + self.dim // 2 + 8
+            return half * (self.cfg.angle_bits + self.cfg.radius_bits) // 8 + 16 * self.value_bits + 8
         vb = 4 if self.value_dtype == torch.float32 else 2
         return half * (self.cfg.angle_bits + self.cfg.radius_bits) // 8 + self.dim * vb
 
@@ -707,6 +709,8 @@ class PackedKVCache:
                 raise ValueError(f"bits must be in [1, 8], got {self.value_bits}")
             if not bool(torch.isfinite(v).all()):  # quantize_uniform, baseline_quant.py:88-89 (before any write)
                 raise ValueError("values contain non-finite entries")
+            if self._dev.value_bits is not None:  # code pages: the store kernel quantizes
+                return v.to(torch.float32)
             out = torch.empty((count, self._dim), dtype=torch.float32, device=dev)
             v = v.contiguous()
             _lib.call("pqb_quantize_values", ptr(v), dtype_code(v), count, self._dim, self.value_bits, ptr(out),
@@ -725,8 +729,11 @@ class PackedKVCache:
         if d < 2 or d % 2:
             raise ValueError(f"vector dimension must be even and >= 2, got {d}")
         self._dim = d
+        # quantized values of 2 / 4 / 8 bits at d = 128 live as code pages (the
+        # decode kernel reads them); other widths as their dequantized fp32 rows
+        vq = self.quantize_values and self.value_bits in VQ_DTYPE and d == 128
         self._dev = PolarKVCache(self.cfg, 1, d, self.residual_len, capacity=max(T + 64, 128), page_tokens=64,
-                                 value_dtype=torch.float32, device=dev)
+                                 value_dtype=torch.float32, device=dev, value_bits=self.value_bits if vq else None)
         try:
             v = self._value_rows(values, T)
             if values is None and self.quantize_values:

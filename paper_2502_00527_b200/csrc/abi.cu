@@ -34,6 +34,8 @@ static int cuda_status(const char* what) {
     }                                    \
   } while (0)
 
+static bool is_vq(int dt) { return dt == PQB_VQ2 || dt == PQB_VQ4 || dt == PQB_VQ8; }
+static int vq_bits_host(int dt) { return dt == PQB_VQ2 ? 2 : dt == PQB_VQ4 ? 4 : dt == PQB_VQ8 ? 8 : 0; }
 static bool dtype_ok(int dt) { return dt == PQB_F32 || dt == PQB_BF16 || dt == PQB_F16; }
 static bool layout_ok(int l) { return l == PQB_ADJACENT || l == PQB_HALF_SPLIT; }
 static int elem_bytes(int dt) { return dt == PQB_F32 ? 4 : 2; }
@@ -63,12 +65,13 @@ static int check_store(const pqb_store* st, int d, int m, int n, bool need_value
             "store: radius region exceeds page");
   if (need_values) {
     PQB_CHECK(st->value_off >= 0, PQB_EINVAL, "store: no value region");
-    PQB_CHECK(st->value_dtype == PQB_F32 || st->value_dtype == PQB_BF16 || st->value_dtype == PQB_VQ4, PQB_EINVAL,
+    PQB_CHECK(st->value_dtype == PQB_F32 || st->value_dtype == PQB_BF16 || is_vq(st->value_dtype), PQB_EINVAL,
               "store: bad value dtype");
-    PQB_CHECK(st->value_dtype != PQB_VQ4 || (d == 128 && st->value_off % 16 == 0), PQB_EUNSUPPORTED,
-              "store: 4-bit values need d = 128 and a 16-byte aligned value region");
+    PQB_CHECK(!is_vq(st->value_dtype) || (d == 128 && st->value_off % 16 == 0), PQB_EUNSUPPORTED,
+              "store: quantized values need d = 128 and a 16-byte aligned value region");
     const int64_t vb = static_cast<int64_t>(st->page_tokens) *
-                       (st->value_dtype == PQB_VQ4 ? 72 : d * (st->value_dtype == PQB_F32 ? 4 : 2));
+                       (is_vq(st->value_dtype) ? 16 * vq_bits_host(st->value_dtype) + 8
+                                               : d * (st->value_dtype == PQB_F32 ? 4 : 2));
     PQB_CHECK(st->value_off + vb <= st->page_bytes, PQB_EINVAL, "store: value region exceeds page");
   }
   return PQB_OK;
@@ -146,10 +149,10 @@ int pqb_store_values_ex(const void* values, int value_dtype, int64_t n_units, in
   PQB_CHECK(d >= 2 && d % 2 == 0, PQB_EINVAL, "vector dimension must be even and >= 2, got %d", d);
   PQB_CHECK(values == nullptr || dtype_ok(value_dtype), PQB_EINVAL, "bad value dtype");
   PQB_CHECK(store && store->pool && store->value_off >= 0, PQB_EINVAL, "store has no value region");
-  PQB_CHECK(store->value_dtype == PQB_F32 || store->value_dtype == PQB_BF16 || store->value_dtype == PQB_VQ4,
+  PQB_CHECK(store->value_dtype == PQB_F32 || store->value_dtype == PQB_BF16 || is_vq(store->value_dtype),
             PQB_EINVAL, "bad store value dtype");
-  PQB_CHECK(store->value_dtype != PQB_VQ4 || (d == 128 && tok_offset == nullptr && tok_offset_const % 32 == 0),
-            PQB_EUNSUPPORTED, "4-bit value stores take d = 128 and whole 32-token tiles");
+  PQB_CHECK(!is_vq(store->value_dtype) || (d == 128 && tok_offset == nullptr && tok_offset_const % 32 == 0),
+            PQB_EUNSUPPORTED, "quantized value stores take d = 128 and whole 32-token tiles");
   PQB_CHECK(n_units >= 0 && n_units <= 65535 && tokens >= 0, PQB_EINVAL, "bad token / unit count");
   if (n_units == 0 || tokens == 0) return PQB_OK;
   launch_store_values(values, value_dtype, n_units, tokens, d, unit_stride, tok_stride, *store, tok_offset,

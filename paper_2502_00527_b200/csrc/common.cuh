@@ -134,28 +134,65 @@ PQB_DEV int64_t value_offset(int64_t t, int e, int d, int value_dtype) {
   return (t * d + e) * 2;
 }
 
-// PQB_VQ4 value pages (d = 128).  Tile = 32 tokens; its 4096 codes are 512
-// words in m16n8k16 A-fragment order of V^T (rows = dims, cols = tokens):
-// word (mt * 2 + ks) * 32 + lane holds, for lane = 4 g + t, the fragment
-// registers a0..a3 of dim block mt and token block ks as nibbles
-//   a_k low half  (token 2t + 8 (k >> 1), dim g + 8 (k & 1)) at bits 4k
-//   a_k high half (token 2t + 1 + 8 (k >> 1), same dim)      at bits 16 + 4k.
-PQB_DEV void vq4_pos(int t_in_tile, int e, int& word, int& shift) {
+// Per-token uniform value codes of b in {2, 4, 8} bits (PQB_VQ2 / PQB_VQ4 /
+// PQB_VQ8; quantize_uniform PER_TOKEN, baseline_quant.py:58-110), d = 128.
+// A 32-token tile's 4096 codes (512 b bytes) are stored in m16n8k16
+// A-fragment order of V^T (rows = dims, cols = tokens), so the decode kernel
+// turns code words straight into MMA registers.  Lane = 4 g + t of dim block
+// mt and token block ks owns 8 codes: register a_k (k = 0..3) low half
+// (token 2t + 8 (k >> 1), dim g + 8 (k & 1)), high half (token + 1, same dim).
+//   b = 4: word (mt * 2 + ks) * 32 + lane; a_k low at bits 4k, high at 16 + 4k.
+//   b = 8: word pair 2 ((mt * 2 + ks) * 32 + lane) + {0, 1}: the low nibbles,
+//          then the high nibbles, each in the b = 4 arrangement.
+//   b = 2: word ((mt * 2 + ks) >> 1) * 32 + lane, half h = (mt * 2 + ks) & 1:
+//          a_k low at bits 16 h + 2k, high at 16 h + 8 + 2k.
+// After the codes, fp32 (zp, scale) per token: [page_tokens][2].
+__host__ __device__ __forceinline__ int vq_bits(int value_dtype) {
+  return value_dtype == PQB_VQ4 ? 4 : value_dtype == PQB_VQ2 ? 2 : value_dtype == PQB_VQ8 ? 8 : 0;
+}
+__host__ __device__ __forceinline__ int vq_tile_bytes(int bits) { return 512 * bits; }
+
+// Word index and bit shift of code (token t_in_tile, dim e); for b = 8 the
+// low nibble's position (the high nibble sits in word + 1 at the same shift).
+PQB_DEV void vq_pos(int bits, int t_in_tile, int e, int& word, int& shift) {
   const int ks = t_in_tile >> 4, tt = t_in_tile & 15, mt = e >> 4, ee = e & 15;
   const int k = (ee >> 3) + 2 * (tt >> 3);
-  word = (mt * 2 + ks) * 32 + (ee & 7) * 4 + ((tt & 7) >> 1);
-  shift = 4 * k + 16 * (tt & 1);
+  const int ln = (ee & 7) * 4 + ((tt & 7) >> 1), c = tt & 1, blk = mt * 2 + ks;
+  if (bits == 2) {
+    word = (blk >> 1) * 32 + ln;
+    shift = 16 * (blk & 1) + 8 * c + 2 * k;
+  } else if (bits == 8) {
+    word = 2 * (blk * 32 + ln);
+    shift = 4 * k + 16 * c;
+  } else {
+    word = blk * 32 + ln;
+    shift = 4 * k + 16 * c;
+  }
 }
-PQB_DEV int64_t vq4_params_off(const pqb_store& st) { return st.value_off + static_cast<int64_t>(st.page_tokens) * 64; }
+PQB_DEV void vq4_pos(int t_in_tile, int e, int& word, int& shift) { vq_pos(4, t_in_tile, e, word, shift); }
 
-// Value (token t of the page, element e) of any value store, as fp32.
+PQB_DEV int64_t vq_params_off(const pqb_store& st) {
+  return st.value_off + static_cast<int64_t>(st.page_tokens) * 16 * vq_bits(st.value_dtype);
+}
+PQB_DEV int64_t vq4_params_off(const pqb_store& st) { return vq_params_off(st); }
+
+// Code of (token t_in_tile, dim e) from a tile's words.
+PQB_DEV uint32_t vq_code(int bits, const uint32_t* tile_words, int t_in_tile, int e) {
+  int w, sh;
+  vq_pos(bits, t_in_tile, e, w, sh);
+  if (bits == 8) return ((tile_words[w] >> sh) & 15u) | (((tile_words[w + 1] >> sh) & 15u) << 4);
+  return (tile_words[w] >> sh) & ((1u << bits) - 1u);
+}
+
+// Value (token t of the page, element e) of any value store, as fp32
+// (quantized: dequantize_uniform's fl(fl(code * scale) + zp), baseline_quant.py:143-167).
 PQB_DEV float load_value(const pqb_store& st, const uint8_t* page, int64_t t, int e, int d) {
-  if (st.value_dtype == PQB_VQ4) {
-    int w, sh;
-    vq4_pos(static_cast<int>(t & 31), e, w, sh);
-    const uint32_t word = reinterpret_cast<const uint32_t*>(page + st.value_off + (t >> 5) * 2048)[w];
-    const float2 zs = reinterpret_cast<const float2*>(page + vq4_params_off(st))[t];
-    return __fadd_rn(__fmul_rn(static_cast<float>((word >> sh) & 15u), zs.y), zs.x);
+  const int vb = vq_bits(st.value_dtype);
+  if (vb) {
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(page + st.value_off + (t >> 5) * vq_tile_bytes(vb));
+    const uint32_t code = vq_code(vb, words, static_cast<int>(t & 31), e);
+    const float2 zs = reinterpret_cast<const float2*>(page + vq_params_off(st))[t];
+    return __fadd_rn(__fmul_rn(static_cast<float>(code), zs.y), zs.x);
   }
   const uint8_t* vp = page + st.value_off + value_offset(t, e, d, st.value_dtype);
   return st.value_dtype == PQB_F32 ? *reinterpret_cast<const float*>(vp)

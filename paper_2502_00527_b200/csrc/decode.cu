@@ -737,7 +737,7 @@ static int dispatch_fast(const DecodeArgs& a, cudaStream_t s, bool& handled) {
 
 int launch_decode(const DecodeArgs& a, cudaStream_t s) {
   const pqb_cache& c = *a.cache;
-  const bool vq = c.store.value_dtype == PQB_VQ4 && a.out != nullptr;  // 4-bit values: DQ kernel or generic
+  const bool vq = vq_bits(c.store.value_dtype) && a.out != nullptr;  // quantized values: DQ kernel or generic
   const bool f32v = c.store.value_dtype == PQB_F32 && a.out != nullptr;  // fp32 values: DQ kernel or generic
   const bool fast_ok = c.d == 128 && (a.out == nullptr || c.store.value_dtype == PQB_BF16 || vq || f32v) &&
                        (a.group == 1 || a.group == 4 || a.group == 8) && c.store.page_tokens % kTile == 0 &&

@@ -90,13 +90,18 @@ static_assert(!kDqWs || kNW == 8, "producer j serves compute warps j and j + 4")
 constexpr int kValBf16 = 0;  // bf16 rows, tensor-core P.V (hi/lo P)
 constexpr int kValVq4 = 1;   // PQB_VQ4: 4-bit per-token codes + (zp, scale), tensor-core P.V
 constexpr int kValF32 = 2;   // PQB_F32: the reference's default fp32 rows (kv_cache.py:8-9, :209), CUDA-core P.V
+constexpr int kValVq2 = 3;   // PQB_VQ2: 2-bit codes, as kValVq4
+constexpr int kValVq8 = 4;   // PQB_VQ8: 8-bit codes as two nibble planes, two MMAs per fragment
+constexpr bool val_is_vq(int v) { return v == kValVq4 || v == kValVq2 || v == kValVq8; }
+constexpr int val_vq_bits(int v) { return v == kValVq2 ? 2 : v == kValVq8 ? 8 : 4; }
 
 template <int G, int M, int N, int VQ = 0>
 struct DqCfg {
   static constexpr int kABytes = kTile * 8 * M;
   static constexpr int kRBytes = kTile * 8 * N;
   // bf16 value rows, 2 KB of fragment-order 4-bit codes + 32 (zp, scale), or fp32 rows
-  static constexpr int kVBytes = VQ == kValVq4 ? 2048 + kTile * 8 : VQ == kValF32 ? kTile * 512 : kTile * 256;
+  static constexpr int kVqCodeBytes = 512 * val_vq_bits(VQ);  // a tile's value codes (quantized modes)
+  static constexpr int kVBytes = val_is_vq(VQ) ? kVqCodeBytes + kTile * 8 : VQ == kValF32 ? kTile * 512 : kTile * 256;
   static constexpr int kStageBytes = kABytes + kRBytes + kVBytes;
   // stages per compute warp: fp32 rows make an 18 KB stage, so one per warp
   // (8 in flight per SM, double the bytes of the bf16 ring's 16 x 10 KB)
@@ -293,11 +298,13 @@ PQB_DEV void issue_tile_dq(uint8_t* st, const pqb_store& s, const uint8_t* pb, i
     bulk_g2s(st + kA, pb + s.radius_off + in_page * 8 * N, kR, bar);
     bulk_g2s(st + kA + kR, pb + s.value_off + static_cast<int64_t>(in_page) * kRow, kV, bar);
   } else {
-    mbar_arrive_expect_tx(bar, kA + kR + 2048 + kTile * 8);
+    constexpr uint32_t kC = 512 * val_vq_bits(VQ);
+    mbar_arrive_expect_tx(bar, kA + kR + kC + kTile * 8);
     bulk_g2s(st, pb + s.angle_off + in_page * 8 * M, kA, bar);
     bulk_g2s(st + kA, pb + s.radius_off + in_page * 8 * N, kR, bar);
-    bulk_g2s(st + kA + kR, pb + s.value_off + tin * 2048, 2048, bar);
-    bulk_g2s(st + kA + kR + 2048, pb + vq4_params_off(s) + in_page * 8, kTile * 8, bar);
+    bulk_g2s(st + kA + kR, pb + s.value_off + static_cast<int64_t>(tin) * kC, kC, bar);
+    bulk_g2s(st + kA + kR + kC, pb + s.value_off + static_cast<int64_t>(s.page_tokens) * (kC / kTile) + in_page * 8,
+             kTile * 8, bar);
   }
 }
 
@@ -327,7 +334,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
                      WorkSplit ws, float* __restrict__ scores, int64_t scores_ld) {
   using Cfg = DqCfg<G, M, N, VQ>;
   constexpr int kSt = Cfg::kSt;
-  constexpr bool kVq4 = VQ == kValVq4, kVf32 = VQ == kValF32;
+  constexpr bool kVq4 = val_is_vq(VQ), kVf32 = VQ == kValF32;  // kVq4: any quantized value mode
+  constexpr int kVqB = val_vq_bits(VQ);
+  constexpr float kVqMid = kVqB == 8 ? 128.0f : kVqB == 4 ? 7.0f : 1.0f;  // ~ half the code range
   constexpr bool kScores = PROBE == kDqScores;
   constexpr bool kFused = M == 4 && N == 4;
   constexpr bool kPacked = Cfg::kPacked;
@@ -564,7 +573,6 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     }
     float m_run = -INFINITY, l_run = 0.0f;  // query g8 (lanes g8 < G)
     float z_run = 0.0f;                     // VQ: sum_t p_t zp_t of query g8 (lane partial)
-    float b_run = 0.0f;                     // VQ: sum_t of the bf16 hi + lo of p_t scale_t fed to the MMA
     float d[8][4];
 #pragma unroll
     for (int mt = 0; mt < 8; ++mt)
@@ -755,7 +763,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           }
         }
       } else {
-      float ls = 0.0f, zs = 0.0f, bs = 0.0f;
+      float ls = 0.0f, zs = 0.0f;
       uint32_t phi[4], plo[4];  // bf16x2 (tokens 8 nb + 2 t4, +1)
 #pragma unroll
       for (int nb = 0; nb < 4; ++nb) {
@@ -763,8 +771,11 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         ls += p0 + p1;
         if constexpr (kVq4) {  // (zp, scale) of tokens 8 nb + 2 t4, +1
           const float4 zsv =
-              reinterpret_cast<const float4*>(st + Cfg::kABytes + Cfg::kRBytes + 2048)[4 * nb + t4];
-          zs = fmaf(p0, zsv.x, fmaf(p1, zsv.z, zs));
+              reinterpret_cast<const float4*>(st + Cfg::kABytes + Cfg::kRBytes + Cfg::kVqCodeBytes)[4 * nb + t4];
+          // centred split: c s + zp = (c - K) s + (zp + K s), K = kVqMid; the MMA
+          // takes c - K (via the tile bias below), the row midpoints go here,
+          // so neither sum carries the rows' common offset
+          zs = fmaf(p0, fmaf(kVqMid, zsv.y, zsv.x), fmaf(p1, fmaf(kVqMid, zsv.w, zsv.z), zs));
           p0 *= zsv.y;
           p1 *= zsv.w;
         }
@@ -773,16 +784,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
         phi[nb] = *reinterpret_cast<const uint32_t*>(&hi);
         plo[nb] = *reinterpret_cast<const uint32_t*>(&lo);
-        if constexpr (kVq4) {
-          const float2 lf = __bfloat1622float2(lo);
-          bs += (hf.x + hf.y) + (lf.x + lf.y);
-        }
       }
       l_run = fmaf(l_run, alpha, ls);
-      if constexpr (kVq4) {
-        z_run = fmaf(z_run, alpha, zs);
-        b_run = fmaf(b_run, alpha, bs);
-      }
+      if constexpr (kVq4) z_run = fmaf(z_run, alpha, zs);
       if (__any_sync(0xffffffffu, rescale && g8 < G)) {
         const float a0 = __shfl_sync(0xffffffffu, alpha, qc0 * 4), a1 = __shfl_sync(0xffffffffu, alpha, qc1 * 4);
 #pragma unroll
@@ -804,21 +808,59 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       // the P^T B-fragments are the score registers (k-step ks = n-blocks 2ks, 2ks+1)
       if constexpr (kVq4) {
         // A fragments straight from the code words: nibble -> bf16 (128 + c) by
-        // OR-ing into the bit pattern of 128.0; the 128 * sum(B) it adds is
-        // removed per query in the epilogue, with sum(B) taken over the exact
-        // bf16 hi + lo values the MMA consumed (b_run), so only fp32
-        // accumulation error (~2^-23 * 128 sum p scale) remains
+        // OR-ing into the bit pattern of 128.0.  The 128 * sum(B) this adds is
+        // removed from the accumulators after every tile, by one more MMA per
+        // k-step with A = -128 against the same B fragments (exactly the
+        // per-column sums of the bf16 hi + lo values consumed), together with
+        // the centring offset K.  Removing the offset only at the end let the
+        // accumulators carry 128 x the result across all tiles (measured
+        // 9e-4 (4-bit) .. 3e-3 (2-bit) relative error at 32K tokens).
+        // 2-bit codes: 16 bits per fragment, byte-spread by one PRMT so each
+        // register's two codes land at bits 2k / 16 + 2k.  8-bit codes: two
+        // nibble planes; the high plane as bf16 (2048 + 16 h) (exact: [2048,
+        // 4096) has spacing 16), so A_lo + A_hi = 2176 + c and both MMAs share
+        // one accumulator (the tile bias below is 2176 sum(B) instead of 128).
         const uint32_t* vw = reinterpret_cast<const uint32_t*>(st + Cfg::kABytes + Cfg::kRBytes);
 #pragma unroll
         for (int mt = 0; mt < 8; ++mt) {
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
-            const uint32_t w = vw[(mt * 2 + ks) * 32 + lane];
             uint32_t a[4];
+            if constexpr (kVqB == 2) {
+              const uint32_t w = __byte_perm(vw[mt * 32 + lane], 0u, ks ? 0x4342u : 0x4140u);
 #pragma unroll
-            for (int k = 0; k < 4; ++k) a[k] = ((w >> (4 * k)) & 0x000F000Fu) | 0x43004300u;
+              for (int k = 0; k < 4; ++k) a[k] = ((w >> (2 * k)) & 0x00030003u) | 0x43004300u;
+            } else {
+              const uint32_t w = kVqB == 8 ? vw[2 * ((mt * 2 + ks) * 32 + lane)] : vw[(mt * 2 + ks) * 32 + lane];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) a[k] = ((w >> (4 * k)) & 0x000F000Fu) | 0x43004300u;
+            }
             mma_bf16(d[mt], a[0], a[1], a[2], a[3], phi[2 * ks], phi[2 * ks + 1]);
             if constexpr (!kPacked) mma_bf16(d[mt], a[0], a[1], a[2], a[3], plo[2 * ks], plo[2 * ks + 1]);
+            if constexpr (kVqB == 8) {
+              const uint32_t wh = vw[2 * ((mt * 2 + ks) * 32 + lane) + 1];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) a[k] = ((wh >> (4 * k)) & 0x000F000Fu) | 0x45004500u;
+              mma_bf16(d[mt], a[0], a[1], a[2], a[3], phi[2 * ks], phi[2 * ks + 1]);
+              if constexpr (!kPacked) mma_bf16(d[mt], a[0], a[1], a[2], a[3], plo[2 * ks], plo[2 * ks + 1]);
+            }
+          }
+        }
+        {  // the tile's bias: -(offset + K) * sum_t B[t][col] (every row alike), added to every dim block
+          // bf16 -(2176 + 128) / -(128 + 7) / -(128 + 1), all exact
+          constexpr uint32_t kNegBias = kVqB == 8 ? 0xC510C510u : kVqB == 4 ? 0xC307C307u : 0xC301C301u;
+          float bias[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            mma_bf16(bias, kNegBias, kNegBias, kNegBias, kNegBias, phi[2 * ks], phi[2 * ks + 1]);
+            if constexpr (!kPacked) mma_bf16(bias, kNegBias, kNegBias, kNegBias, kNegBias, plo[2 * ks], plo[2 * ks + 1]);
+          }
+#pragma unroll
+          for (int mt = 0; mt < 8; ++mt) {
+            d[mt][0] += bias[0];
+            d[mt][1] += bias[1];
+            d[mt][2] += bias[2];
+            d[mt][3] += bias[3];
           }
         }
       } else {
@@ -862,12 +904,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) d[mt][k] += __shfl_xor_sync(0xffffffffu, d[mt][k], 2);
     }
-    if constexpr (kVq4) {  // + sum_t p_t zp_t - 128 sum_t B_t of the column's query
+    if constexpr (kVq4) {  // + sum_t p_t zp_t of the column's query
       z_run += __shfl_xor_sync(0xffffffffu, z_run, 1);
       z_run += __shfl_xor_sync(0xffffffffu, z_run, 2);
-      b_run += __shfl_xor_sync(0xffffffffu, b_run, 1);
-      b_run += __shfl_xor_sync(0xffffffffu, b_run, 2);
-      z_run = fmaf(-128.0f, b_run, z_run);
       const float z0 = __shfl_sync(0xffffffffu, z_run, qc0 * 4), z1 = __shfl_sync(0xffffffffu, z_run, qc1 * 4);
 #pragma unroll
       for (int mt = 0; mt < 8; ++mt) {
@@ -985,6 +1024,14 @@ static int dispatch_dq_mn(const DecodeArgs& a, const EpiArgs& ep, const WorkSpli
       case 42: return launch_dq<G, 4, 2, 0, kValVq4>(a, ep, ws, grid, s);
       case 24: return launch_dq<G, 2, 4, 0, kValVq4>(a, ep, ws, grid, s);
       case 34: return launch_dq<G, 3, 4, 0, kValVq4>(a, ep, ws, grid, s);
+      default: handled = false; return PQB_OK;
+    }
+  }
+  if (a.cache->store.value_dtype == PQB_VQ2 || a.cache->store.value_dtype == PQB_VQ8) {
+    const bool b8 = a.cache->store.value_dtype == PQB_VQ8;
+    switch (mn) {  // the configs' shapes; other (m, n) take the generic kernel
+      case 44: return b8 ? launch_dq<G, 4, 4, 0, kValVq8>(a, ep, ws, grid, s) : launch_dq<G, 4, 4, 0, kValVq2>(a, ep, ws, grid, s);
+      case 32: return b8 ? launch_dq<G, 3, 2, 0, kValVq8>(a, ep, ws, grid, s) : launch_dq<G, 3, 2, 0, kValVq2>(a, ep, ws, grid, s);
       default: handled = false; return PQB_OK;
     }
   }

@@ -671,16 +671,18 @@ __global__ void store_values_kernel(const void* __restrict__ vals, int src_dtype
   }
 }
 
-// PQB_VQ4 pages: _quantize_slices along each token row (baseline_quant.py:58-66:
-// zp = min, scale = fl(fl(max - zp) / 15), code = rint(fl(fl(v - zp) / scale))
-// clipped to [0, 15], scale == 0 -> 0), written in the fragment order of
-// vq4_pos().  One CTA per (32-token tile, unit); tile starts are 32-aligned.
-__global__ void __launch_bounds__(256) store_values_vq4_kernel(const void* __restrict__ vals, int src_dtype,
+// PQB_VQ{2,4,8} pages: _quantize_slices along each token row (baseline_quant.py:58-66:
+// zp = min, scale = fl(fl(max - zp) / (2^b - 1)), code = rint(fl(fl(v - zp) / scale))
+// clipped to [0, 2^b - 1], scale == 0 -> 0), written in the fragment order of
+// vq_pos().  One CTA per (32-token tile, unit); tile starts are 32-aligned.
+__global__ void __launch_bounds__(256) store_values_vq_kernel(const void* __restrict__ vals, int src_dtype,
                                                                int64_t T, int64_t unit_stride, int64_t tok_stride,
                                                                pqb_store st, int64_t tok_offset_const,
                                                                int32_t* __restrict__ flags) {
   __shared__ uint8_t codes[32][132];
   __shared__ float2 params[32];
+  const int bits = vq_bits(st.value_dtype);
+  const float top = static_cast<float>((1 << bits) - 1);
   const int64_t unit = blockIdx.y;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -704,11 +706,11 @@ __global__ void __launch_bounds__(256) store_values_vq4_kernel(const void* __res
       mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     }
-    const float scale = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
+    const float scale = __fdiv_rn(__fsub_rn(mx, mn), top);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       float raw = scale == 0.0f ? 0.0f : rintf(__fdiv_rn(__fsub_rn(v[k], mn), scale));
-      raw = fminf(fmaxf(raw, 0.0f), 15.0f);
+      raw = fminf(fmaxf(raw, 0.0f), top);
       codes[r][lane + 32 * k] = t < T ? static_cast<uint8_t>(raw) : 0;
     }
     if (lane == 0) params[r] = t < T ? make_float2(mn, scale) : make_float2(0.0f, 0.0f);
@@ -718,20 +720,31 @@ __global__ void __launch_bounds__(256) store_values_vq4_kernel(const void* __res
   const int64_t page = ta / st.page_tokens;
   const int64_t tp = ta - page * st.page_tokens;  // multiple of 32
   uint8_t* pb = page_base(st, unit, page);
-  uint32_t* wout = reinterpret_cast<uint32_t*>(pb + st.value_off + (tp >> 5) * 2048);
-  for (int w = threadIdx.x; w < 512; w += blockDim.x) {
-    const int mt = w >> 6, ks = (w >> 5) & 1, ln = w & 31, g = ln >> 2, tq = ln & 3;
-    uint32_t word = 0u;
+  uint32_t* wout = reinterpret_cast<uint32_t*>(pb + st.value_off + (tp >> 5) * vq_tile_bytes(bits));
+  // one thread per (dim block, token block, lane) chunk of 8 codes: its words
+  // (b = 4: one, b = 8: two, b = 2: one half word) in vq_pos() order
+  for (int i = threadIdx.x; i < 512; i += blockDim.x) {
+    const int blk = i >> 5, mt = blk >> 1, ks = blk & 1, ln = i & 31, g = ln >> 2, tq = ln & 3;
+    uint32_t lo = 0u, hi = 0u, two = 0u;
 #pragma unroll
     for (int k = 0; k < 4; ++k)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         const int t = 16 * ks + 2 * tq + c + 8 * (k >> 1), e = 16 * mt + g + 8 * (k & 1);
-        word |= static_cast<uint32_t>(codes[t][e]) << (4 * k + 16 * c);
+        const uint32_t code = codes[t][e];
+        lo |= (code & 15u) << (4 * k + 16 * c);
+        hi |= (code >> 4) << (4 * k + 16 * c);
+        two |= code << (8 * c + 2 * k);
       }
-    wout[w] = word;
+    if (bits == 4) {
+      wout[i] = lo;
+    } else if (bits == 8) {
+      reinterpret_cast<uint2*>(wout)[i] = make_uint2(lo, hi);
+    } else {  // b = 2: blocks 2j, 2j + 1 share word j * 32 + lane (low / high half)
+      reinterpret_cast<uint16_t*>(wout)[2 * ((blk >> 1) * 32 + ln) + (blk & 1)] = static_cast<uint16_t>(two);
+    }
   }
-  if (threadIdx.x < 32) reinterpret_cast<float2*>(pb + vq4_params_off(st))[tp + threadIdx.x] = params[threadIdx.x];
+  if (threadIdx.x < 32) reinterpret_cast<float2*>(pb + vq_params_off(st))[tp + threadIdx.x] = params[threadIdx.x];
   if (bad && flags) atomicOr(flags, PQB_FLAG_NONFINITE);
 }
 
@@ -757,11 +770,11 @@ __global__ void store_residual_kernel(const void* __restrict__ keys, int src_dty
 
 // ----------------------------------------------------------------- K5
 
-// One token's value row into a PQB_VQ4 page (append): quantize as
-// store_values_vq4_kernel, OR the nibbles into the tile's words (pages start
+// One token's value row into a PQB_VQ{2,4,8} page (append): quantize as
+// store_values_vq_kernel, OR the code bits into the tile's words (pages start
 // zeroed and every token slot is written once).  red: >= 2 * 32 floats of
 // shared scratch.  Caller: the whole block (d = 128 threads or more).
-__device__ void append_value_vq4(const pqb_cache& c, int64_t unit, int64_t T, const void* vals, int val_dtype,
+__device__ void append_value_vq(const pqb_cache& c, int64_t unit, int64_t T, const void* vals, int val_dtype,
                                  float* red, bool& bad) {
   const int e = threadIdx.x, lane = e & 31, warp = e >> 5, nw = (blockDim.x + 31) >> 5;
   float v = 0.0f;
@@ -787,18 +800,23 @@ __device__ void append_value_vq4(const pqb_cache& c, int64_t unit, int64_t T, co
     mn = fminf(mn, red[w]);
     mx = fmaxf(mx, red[32 + w]);
   }
-  const float scale = __fdiv_rn(__fsub_rn(mx, mn), 15.0f);
+  const int vb = vq_bits(c.store.value_dtype);
+  const float top = static_cast<float>((1 << vb) - 1);
+  const float scale = __fdiv_rn(__fsub_rn(mx, mn), top);
   const int64_t page = T / c.store.page_tokens, tp = T - page * c.store.page_tokens;
   uint8_t* pb = page_base(c.store, unit, page);
   if (e < 128) {
     float raw = scale == 0.0f ? 0.0f : rintf(__fdiv_rn(__fsub_rn(v, mn), scale));
-    raw = fminf(fmaxf(raw, 0.0f), 15.0f);
+    raw = fminf(fmaxf(raw, 0.0f), top);
     int w, sh;
-    vq4_pos(static_cast<int>(tp & 31), e, w, sh);
-    const uint32_t bits = static_cast<uint32_t>(raw) << sh;
-    if (bits) atomicOr(reinterpret_cast<unsigned int*>(pb + c.store.value_off + (tp >> 5) * 2048) + w, bits);
+    vq_pos(vb, static_cast<int>(tp & 31), e, w, sh);
+    const uint32_t code = static_cast<uint32_t>(raw);
+    unsigned int* words = reinterpret_cast<unsigned int*>(pb + c.store.value_off + (tp >> 5) * vq_tile_bytes(vb));
+    const uint32_t b0 = (vb == 8 ? (code & 15u) : code) << sh;
+    if (b0) atomicOr(words + w, b0);
+    if (vb == 8 && (code >> 4)) atomicOr(words + w + 1, (code >> 4) << sh);
   }
-  if (e == 0) reinterpret_cast<float2*>(pb + vq4_params_off(c.store))[tp] = make_float2(mn, scale);
+  if (e == 0) reinterpret_cast<float2*>(pb + vq_params_off(c.store))[tp] = make_float2(mn, scale);
   __syncthreads();
 }
 
@@ -831,14 +849,14 @@ __global__ void __launch_bounds__(256) append_kernel(pqb_cache c, const void* __
                          clamps, bad);
   }
   __syncthreads();  // the flushed slot is read before it is overwritten
-  if (c.store.value_dtype == PQB_VQ4) append_value_vq4(c, unit, T, vals, val_dtype, s_scale + half, bad);
+  if (vq_bits(c.store.value_dtype)) append_value_vq(c, unit, T, vals, val_dtype, s_scale + half, bad);
   for (int e = threadIdx.x; e < d; e += blockDim.x) {
     const int64_t ko = unit * d + e;
     const float kv = key_dtype == PQB_F32 ? load1<PQB_F32>(keys, ko)
                                           : (key_dtype == PQB_BF16 ? load1<PQB_BF16>(keys, ko) : load1<PQB_F16>(keys, ko));
     bad |= !(fabsf(kv) <= 3.40282347e38f);
     if (c.res_cap > 0) c.residual[(unit * c.res_cap + T % c.res_cap) * d + e] = kv;
-    if (c.store.value_off >= 0 && c.store.value_dtype != PQB_VQ4) {
+    if (c.store.value_off >= 0 && !vq_bits(c.store.value_dtype)) {
       float v = 0.0f;
       if (vals)
         v = val_dtype == PQB_F32 ? load1<PQB_F32>(vals, ko)
@@ -1012,9 +1030,9 @@ int launch_store_values(const void* vals, int dtype, int64_t n_units, int64_t T,
                         const pqb_store& st, const int32_t* tok_offset, int64_t tok_offset_const, cudaStream_t s,
                         int32_t* flags) {
   if (T == 0) return 0;
-  if (st.value_dtype == PQB_VQ4) {
+  if (st.value_dtype == PQB_VQ4 || st.value_dtype == PQB_VQ2 || st.value_dtype == PQB_VQ8) {
     dim3 grid(static_cast<unsigned>((T + 31) / 32), static_cast<unsigned>(n_units));
-    store_values_vq4_kernel<<<grid, 256, 0, s>>>(vals, dtype, T, us, ts, st, tok_offset_const, flags);
+    store_values_vq_kernel<<<grid, 256, 0, s>>>(vals, dtype, T, us, ts, st, tok_offset_const, flags);
     return 0;
   }
   const int eb = dtype == PQB_F32 ? 4 : 2;

@@ -122,11 +122,12 @@ def test_values_and_value_quant_mode():
 def test_value_quant_mode_bit_exact_vs_reference_semantics():
     """Per-token uniform quantize->dequantize (baseline_quant.py:58-110, 167)."""
     rng = np.random.default_rng(4)
-    v = rng.standard_normal((50, 32)).astype(np.float32)
-    v[3] = 1.5  # constant row -> scale 0 -> exact zero-point
-    for bits in (2, 4, 8):
+    for dim, bits in [(32, 2), (32, 4), (32, 8), (128, 2), (128, 4), (128, 8), (128, 3)]:
+        # d = 128 with 2 / 4 / 8 bits: code pages read by the decode kernels
+        v = rng.standard_normal((50, dim)).astype(np.float32)
+        v[3] = 1.5  # constant row -> scale 0 -> exact zero-point
         c = pq.PackedKVCache(pq.QuantConfig(4, 4), 0, quantize_values=True, value_bits=bits)
-        c.prefill(_keys(50, dim=32), v)
+        c.prefill(_keys(50, dim=dim), v)
         top = (1 << bits) - 1
         zp = v.min(axis=1, keepdims=True)
         scale = (v.max(axis=1, keepdims=True) - zp) / top

@@ -68,8 +68,10 @@ def test_configs3_g8_separate_merge():
     assert launches == 2
 
 
-def test_configs1_vq4_values():
-    summ, _ = _run_layer(batch=16, hq=32, hkv=8, T=32768, m=4, n=4, values="vq4", keep=[0, 7, 64, 127])
+@pytest.mark.parametrize("values", ["vq2", "vq4", "vq8"])
+def test_configs1_quantized_values(values):
+    """The reference's per-token value quantization (kv_cache.py:199-209) at 2 / 4 / 8 bits."""
+    summ, _ = _run_layer(batch=16, hq=32, hkv=8, T=32768, m=4, n=4, values=values, keep=[0, 7, 64, 127])
     _assert_ok(summ, 4)
 
 
@@ -95,3 +97,34 @@ def test_bench_two_ranks(shard):
     assert d["n_gpus"] == 2
     assert d["parity"]["passed"] and d["parity"]["ranks"] == 2
     assert d["e2e"]["value"] <= d["value"] * 1.10  # host copies inside the timed region (noise allowance)
+
+
+@pytest.mark.parametrize("values", ["bf16", "f32", "vq2", "vq4", "vq8"])
+def test_fp32_outputs_at_32k(values):
+    """fp32 outputs of the fused decode at the bench's context length for every
+    value treatment: max |o - ref| <= 1e-4 max(1, max |ref|) against
+    softmax64(LUT scores) . values() (the quantized modes remove their code
+    offset per tile and split off the rows' midpoints, see decode_dq.cu)."""
+    import math
+
+    import numpy as np
+    import torch
+
+    import bench
+    from oracle import exact, polar_oracle as po
+
+    dev = torch.device("cuda", 0)
+    keep = list(range(0, 128, 16))
+    w = bench.DecodeWorkload(dev, layers=1, batch=16, hq=32, hkv=8, T=32768, m=4, n=4, page_tokens=256, seed=7,
+                             values=values, keep=keep)
+    o32 = w.views[0].decode(w.q[0], out_dtype=torch.float32).cpu().numpy()
+    for u in keep:
+        _, vv = w.kept[u]
+        v64 = (w.cache.values_f32(u) if values.startswith("vq") else vv.float()).cpu().numpy().astype(np.float64)
+        a, r = (t.cpu().numpy() for t in w.cache.code_arrays(u))
+        s16 = w.cache.scales16[u].cpu().numpy()
+        q = w.q[0, u].float().cpu().numpy()
+        for g in range(4):
+            ref = po.softmax64(exact.lut_scores(q[g], a, r, s16, 4, 4, 1), 1 / math.sqrt(128)) @ v64
+            assert np.abs(o32[u, g] - ref).max() <= 1e-4 * max(1.0, float(np.abs(ref).max()))
+    w.free()

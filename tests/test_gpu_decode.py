@@ -343,7 +343,7 @@ def test_dq_extreme_scales_and_zero_query():
 # ---------------------------------------------------------------- 4-bit values
 
 
-def _vq4_cache(m, n, lay, res, lens, G, seed, shuffle=False):
+def _vq4_cache(m, n, lay, res, lens, G, seed, shuffle=False, bits=4):
     U = len(lens)
     T = max(lens)
     keys = [po.synthetic_keys(t, 128, seed=seed + u, outliers=(0, 1), layout=lay) for u, t in enumerate(lens)]
@@ -353,7 +353,7 @@ def _vq4_cache(m, n, lay, res, lens, G, seed, shuffle=False):
         v[min(3, len(v) - 1)] = 0.25
         v[len(v) // 2] *= 50.0
     q = rng.standard_normal((U, G, 128)).astype(np.float32)
-    cache = pq.PolarKVCache(pq.QuantConfig(m, n, LAY[lay]), U, 128, res, capacity=T + 8, value_bits=4,
+    cache = pq.PolarKVCache(pq.QuantConfig(m, n, LAY[lay]), U, 128, res, capacity=T + 8, value_bits=bits,
                             shuffle_pages=shuffle)
     for u in range(U):
         cache.prefill(torch.from_numpy(keys[u]).cuda().unsqueeze(0), torch.from_numpy(vals[u]).cuda().unsqueeze(0),
@@ -361,9 +361,9 @@ def _vq4_cache(m, n, lay, res, lens, G, seed, shuffle=False):
     return cache, keys, vals, q
 
 
-def _vq4_check(cache, keys, vals, q, m, n, lay, res, lens, outs, tol=OUT_RTOL_F32):
+def _vq4_check(cache, keys, vals, q, m, n, lay, res, lens, outs, tol=OUT_RTOL_F32, bits=4):
     for u, t_u in enumerate(lens):
-        codes, zp, sc = po.quantize_values(vals[u], 4)
+        codes, zp, sc = po.quantize_values(vals[u], bits)
         deq = po.dequantize_values(codes, zp, sc)
         got = cache.values_f32(u).cpu().numpy()
         assert np.array_equal(got.view(np.uint32), deq.view(np.uint32))  # values() bit-identical
@@ -416,9 +416,46 @@ def test_vq4_append_and_bf16_out():
     peak_close(ob, out, 2.0 ** -7)
 
 
+@pytest.mark.parametrize("bits", [2, 8])
+@pytest.mark.parametrize("m,n", [(4, 4), (3, 2), (2, 4)])
+@pytest.mark.parametrize("G", [4, 8])
+@pytest.mark.parametrize("lay,res", [(1, 0), (0, 40)])
+def test_vq2_vq8_decode_vs_oracle(bits, m, n, G, lay, res):
+    """2- and 8-bit per-token values (kv_cache.py:206-207 with value_bits 2 / 8)
+    as code pages read inside the DQ kernel (m4n4, m3n2; other shapes by the
+    generic kernel): values() bit-identical to the reference quantizer, fused
+    output within the fp32 tolerance of softmax64(LUT scores) . values()."""
+    lens = [3000, 1777, 33]
+    cache, keys, vals, q = _vq4_cache(m, n, lay, res, lens, G, seed=500 + bits + 10 * m + n, shuffle=True,
+                                      bits=bits)
+    qd = torch.from_numpy(q).cuda()
+    out = cache.decode(qd).cpu().numpy()
+    gen = cache.decode(qd, flags=pq._lib.PQB_DECODE_FORCE_GENERIC).cpu().numpy()
+    lin = cache._all().decode(qd, flags=pq._lib.PQB_DECODE_DQ | pq._lib.PQB_DECODE_DQ_LINEAR).cpu().numpy()
+    _vq4_check(cache, keys, vals, q, m, n, lay, res, lens, [out, gen, lin], bits=bits)
+
+
+@pytest.mark.parametrize("bits", [2, 8])
+def test_vq2_vq8_append(bits):
+    lens = [500, 257]
+    m, n, lay, res = 4, 4, 1, 16
+    cache, keys, vals, q = _vq4_cache(m, n, lay, res, lens, 4, seed=79, bits=bits)
+    rng = np.random.default_rng(6)
+    for _ in range(40):
+        k_new = rng.standard_normal((2, 128)).astype(np.float32)
+        v_new = rng.standard_normal((2, 128)).astype(np.float32)
+        cache.append(torch.from_numpy(k_new).cuda(), torch.from_numpy(v_new).cuda())
+        for u in range(2):
+            keys[u] = np.concatenate([keys[u], k_new[u:u + 1]])
+            vals[u] = np.concatenate([vals[u], v_new[u:u + 1]])
+    lens = [len(v) for v in vals]
+    out = cache.decode(torch.from_numpy(q).cuda()).cpu().numpy()
+    _vq4_check(cache, keys, vals, q, m, n, lay, res, lens, [out], bits=bits)
+
+
 def test_vq4_rejects_other_widths():
     with pytest.raises(ValueError):
-        pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 128, 0, value_bits=2)
+        pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 128, 0, value_bits=3)
     with pytest.raises(ValueError):
         pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 64, 0, value_bits=4)
 

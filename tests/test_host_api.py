@@ -130,6 +130,6 @@ def test_value_bits_validation_without_gpu():
     with pytest.raises(ValueError):
         pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 128, 0, value_bits=9)
     with pytest.raises(ValueError):
-        pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 128, 0, value_bits=2)
+        pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 128, 0, value_bits=3)
     with pytest.raises(ValueError):
         pq.PolarKVCache(pq.QuantConfig(4, 4), 1, 64, 0, value_bits=4)
