@@ -123,6 +123,31 @@ struct DqCfg {
   static_assert(kNW * kSt * kStageBytes >= kNW * G * 132 * 4, "merge area");
 };
 
+// PQB_DQ_TRACE=1 (probe builds only): consumer thread 0 of every CTA stamps
+// %globaltimer at the launch phases into pqb_dq_trace[cta][32] (read back by
+// pqb_debug_dq_trace; scripts/trace_probe.py): [0] entry, [1] after the grid
+// dependency wait, per segment k < 6: [2+4k] unit setup done, [3+4k] tile loop
+// done, [4+4k] epilogue (incl. a last-CTA merge) done, [5+4k] unit; [31] exit.
+#ifndef PQB_DQ_TRACE
+#define PQB_DQ_TRACE 0
+#endif
+#if PQB_DQ_TRACE
+__device__ unsigned long long pqb_dq_trace[1024 * 32];
+PQB_DEV void trace_stamp(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  pqb_dq_trace[blockIdx.x * 32 + slot] = t;
+}
+#define DQ_TRACE(cond, slot) \
+  do {                       \
+    if (cond) trace_stamp(slot); \
+  } while (0)
+#else
+#define DQ_TRACE(cond, slot) \
+  do {                       \
+  } while (0)
+#endif
+
 PQB_DEV uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
 // PQB_DQ_PRMT_TAB=1 (default; A/B +1.3% G = 4, +2.9% G = 8, all decode tests
@@ -343,6 +368,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   static_assert(G == 1 || G == 2 || G == 4 || G == 8, "G");
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  DQ_TRACE(tid == 0, 0);
 #if PQB_DQ_PRMT_TAB
   const int tab_off = static_cast<int>(kPtTabAbs - smem_u32(smem));  // dynamic offset of the table
   const int n_before = tab_off / Cfg::kStageBytes;                     // stages before the table
@@ -424,11 +450,14 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   // this grid's predecessors to complete.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  DQ_TRACE(tid == 0, 1);
   const int tpp = c.store.page_tokens / kTile;  // tiles per page
   const int dpg = kNW / tpp, dtin = kNW - (kNW / tpp) * tpp;  // cursor step of kNW tiles
   const int64_t i_begin = static_cast<int64_t>(blockIdx.x) * ws.per_cta;
   const int64_t i_end = min(ws.items, i_begin + ws.per_cta);
   uint32_t k_iter = 0;
+  int n_seg_tr = 0;  // PQB_DQ_TRACE: segment index
+  (void)n_seg_tr;
 
   if constexpr (kDqWs) {
     if (warp >= kNW) {  // ---- producer warpgroup
@@ -554,6 +583,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       aq[ks][3] = v.w;
     }
     const float xscale = ldexpf(sm_scale_log2, -e_sc);
+    DQ_TRACE(tid == 0 && n_seg_tr < 6, 2 + 4 * n_seg_tr);
+#if PQB_DQ_TRACE
+    if (tid == 0 && n_seg_tr < 6) pqb_dq_trace[blockIdx.x * 32 + 5 + 4 * n_seg_tr] = unit;
+#endif
 
     // ---- lane 0 fills this warp's ring with its first tiles
     TileCursor cur;
@@ -896,6 +929,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       continue;
     }
     // ---- segment epilogue: per-warp (m, l, o) -> shared, then the common merge
+    DQ_TRACE(tid == 0 && n_seg_tr < 6, 3 + 4 * n_seg_tr);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
     if constexpr (kPacked && !kVf32) {  // O = columns q (P_hi) + q + 4 (P_lo): lanes t4, t4 ^ 2
@@ -942,8 +976,11 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     }
     finish_segment<G>(ep, ws, unit, red, s_misc + 1, tid, kConsThreads);
     if constexpr (kDqWs) named_arrive(2, kDqThreads);  // producers may refill the stages
+    DQ_TRACE(tid == 0 && n_seg_tr < 6, 4 + 4 * n_seg_tr);
+    ++n_seg_tr;
   }
   peer_publish(ep, ep.counters + ws.items / ws.tiles_max, tid, kConsThreads);
+  DQ_TRACE(tid == 0, 31);
 }
 
 // ------------------------------------------------------------------ host side
@@ -1058,6 +1095,13 @@ static int dispatch_dq_mn(const DecodeArgs& a, const EpiArgs& ep, const WorkSpli
     default: handled = false; return PQB_OK;
   }
 }
+
+#if PQB_DQ_TRACE && PQB_DQ_PRMT_TAB
+extern "C" int pqb_debug_dq_trace(void* host, int n_ctas) {
+  return cudaMemcpyFromSymbol(host, pqb_dq_trace, sizeof(unsigned long long) * 32 * std::min(n_ctas, 1024)) ==
+                 cudaSuccess ? 0 : -1;
+}
+#endif
 
 int launch_decode_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s,
                      bool& handled) {

@@ -2,7 +2,7 @@
 # the two-rank peer gather; logs in gpurun_out/san/.
 mkdir -p gpurun_out/san
 CS="compute-sanitizer --print-limit 20 --error-exitcode 9"
-CASES="encode decode_g4 decode_g8 decode_m3n2 decode_vq4 decode_f32v scores append_residual"
+CASES="encode decode_g4 decode_g8 decode_m3n2 decode_vq4 decode_vq28 decode_f32v scores append_residual"
 for tool in memcheck synccheck racecheck; do
   for c in $CASES; do
     timeout 900 $CS --tool $tool python scripts/sanitize.py $c > gpurun_out/san/${tool}_${c}.log 2>&1

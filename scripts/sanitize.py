@@ -68,6 +68,16 @@ def case_decode_vq4():
     c.decode(q)
 
 
+def case_decode_vq28():
+    for vb in (2, 8):
+        c = _cache(4, 4, 3, 4096, vb=vb)
+        q = pq.normal_device((3, 4, 128), 12, dtype=torch.bfloat16)
+        c.decode(q)
+        c = _cache(3, 2, 2, 3000, vb=vb)
+        q = pq.normal_device((2, 8, 128), 13, dtype=torch.bfloat16)
+        c.decode(q)
+
+
 def case_decode_f32v():
     c = _cache(4, 4, 3, 4096, vdt=torch.float32)
     q = pq.normal_device((3, 4, 128), 9, dtype=torch.bfloat16)
