@@ -623,6 +623,9 @@ def run_ours(a, rank: int, world: int, dist) -> dict | None:
         "step_frac": step_frac,
         "traffic": ncu_traffic() if a.values == "bf16" and a.m == 4 and a.n == 4 and G == 4 else None,
     })
+    if kern.startswith("decode_dq"):  # 1: the product table at its fixed shared address (the fast build)
+        roof["dq_smem_layout"] = {0: "none", 1: "prmt_table", 2: "linear_fallback"}[
+            int(_lib.load().pqb_decode_dq_layout())]
     res = {
         "ms_per_step": ms_step,
         "value": global_batch / (ms_step * 1e-3),

@@ -250,6 +250,11 @@ int pqb_decode_splits(int64_t n_units, int max_tokens);
 /* Kernels one fused DQ decode call (group 4 or 8, out != NULL, no peers) enqueues
  * for this shape and flags: 1, or 2 when the split merge runs as its own launch. */
 int pqb_decode_launches(int64_t n_units, int group, int max_tokens, int flags);
+/* Shared-memory layout the last fused DQ launch in this process used: 0 none
+ * yet, 1 the product table at its fixed shared-window address (the fast
+ * build), 2 the linear-layout fallback (a device whose shared window is laid
+ * out other than measured).  Diagnostics: tests and the bench assert 1. */
+int pqb_decode_dq_layout(void);
 
 /* ------------------------------------------------------------ accessors ----
  * Tables and views the reference API exposes (all computed on the device). */

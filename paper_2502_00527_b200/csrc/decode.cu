@@ -696,6 +696,9 @@ int decode_launch_count(int64_t n_units, int group, int max_tokens, int flags) {
   return (flags & PQB_DECODE_NO_COMBINE) || !separate_merge(flags, group, max_tokens, ws) ? 1 : 2;
 }
 
+static std::atomic<int> g_dq_layout{0};
+int decode_dq_layout() { return g_dq_layout.load(std::memory_order_relaxed); }
+
 static int launch_dq_path(const DecodeArgs& a, cudaStream_t s, bool& handled) {
   EpiArgs ep;
   WorkSplit ws;
@@ -709,7 +712,12 @@ static int launch_dq_path(const DecodeArgs& a, cudaStream_t s, bool& handled) {
                    separate_merge(a.flags, a.group, a.max_tokens, ws);
   if (sep) ep.merge = false;
   int rc2 = (a.flags & PQB_DECODE_DQ_LINEAR) ? kDqLayoutUnavailable : dq_prmt::launch_decode_dq(a, ep, ws, grid, s, handled);
-  if (rc2 == kDqLayoutUnavailable) rc2 = dq_lin::launch_decode_dq(a, ep, ws, grid, s, handled);
+  int layout = 1;
+  if (rc2 == kDqLayoutUnavailable) {
+    rc2 = dq_lin::launch_decode_dq(a, ep, ws, grid, s, handled);
+    layout = 2;
+  }
+  if (rc2 == PQB_OK && handled) g_dq_layout.store(layout, std::memory_order_relaxed);
   if (rc2 != PQB_OK || !handled || !sep) return rc2;
   return launch_merge_split(ep, ws, a.n_units, s);
 }

@@ -981,6 +981,14 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   }
   peer_publish(ep, ep.counters + ws.items / ws.tiles_max, tid, kConsThreads);
   DQ_TRACE(tid == 0, 31);
+#if PQB_DQ_TRACE
+  if (tid == 0) {
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    pqb_dq_trace[blockIdx.x * 32 + 30] = smid;
+    pqb_dq_trace[blockIdx.x * 32 + 29] = static_cast<unsigned long long>(i_end - i_begin);
+  }
+#endif
 }
 
 // ------------------------------------------------------------------ host side

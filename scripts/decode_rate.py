@@ -15,7 +15,7 @@ from paper_2502_00527_b200 import _lib
 dev = torch.device("cuda", 0)
 res = {}
 for name, kw in [("g4", dict(batch=16, hq=32, hkv=8, m=4, n=4)), ("g8", dict(batch=32, hq=8, hkv=1, m=4, n=4)),
-                 ("vq4", dict(batch=16, hq=32, hkv=8, m=4, n=4, value_bits=4)),
+                 ("vq4", dict(batch=16, hq=32, hkv=8, m=4, n=4, values="vq4")),
                  ("m3n2", dict(batch=8, hq=32, hkv=8, m=3, n=2))]:
     T = 131072 if name == "m3n2" else 32768
     w = bench.DecodeWorkload(dev, layers=8, T=T, page_tokens=int(os.environ.get("PQB_PAGE", 128)), seed=0, **kw)

@@ -5,8 +5,9 @@
 Runs the configs[3]- (g8: 32 units of 8 query heads, 32K) or configs[1]-shaped
 (g4: 128 units of 4, 32K) decode step in a CUDA graph (8 layers, PDL between
 launches) and reads back the %globaltimer stamps of the last layer's launch:
-per CTA entry, grid-dependency wait, per segment setup / tile loop / epilogue,
-exit.  Prints a JSON summary of where the launch time goes."""
+per CTA entry, grid-dependency wait, per run of warp 0 setup / tile loop /
+flush, exit, SM id.  Saves the stamps (gpurun_out/trace_<shape>.npy) for
+scripts/trace_summary.py."""
 import ctypes
 import json
 import os
@@ -37,33 +38,6 @@ buf = np.zeros((n, 32), dtype=np.uint64)
 step()
 torch.cuda.synchronize()
 assert lib.pqb_debug_dq_trace(buf.ctypes.data, n) == 0
-t = buf.astype(np.int64)
-t0 = t[:, 0].min()
-rel = (t - t0) / 1e3  # us
-segs = []
-for c in range(n):
-    k = 0
-    while k < 6 and t[c, 2 + 4 * k] != 0 and t[c, 4 + 4 * k] >= t[c, 2 + 4 * k]:
-        prev = t[c, 1] if k == 0 else t[c, 4 + 4 * (k - 1)]
-        segs.append({"cta": c, "k": k, "unit": int(t[c, 5 + 4 * k]),
-                     "setup_us": (t[c, 2 + 4 * k] - prev) / 1e3,
-                     "loop_us": (t[c, 3 + 4 * k] - t[c, 2 + 4 * k]) / 1e3,
-                     "epi_us": (t[c, 4 + 4 * k] - t[c, 3 + 4 * k]) / 1e3})
-        k += 1
-ends = rel[:, 31]
-waits = rel[:, 1]
-pct = lambda a: {p: round(float(np.percentile(a, p)), 2) for p in (0, 10, 50, 90, 100)}
-res = {
-    "shape": shape, "layer_us_graph": round(ms * 1e3, 2),
-    "entry_us": pct(rel[:, 0]), "wait_done_us": pct(waits), "exit_us": pct(ends),
-    "span_us": round(float(ends.max()), 2),
-    "segments_per_cta": pct(np.bincount([s["cta"] for s in segs], minlength=n)),
-    "setup_us": pct([s["setup_us"] for s in segs]),
-    "loop_us": pct([s["loop_us"] for s in segs]),
-    "epi_us": pct([s["epi_us"] for s in segs]),
-    "epi_first_seg_us": pct([s["epi_us"] for s in segs if s["k"] == 0]),
-    "epi_last_seg_us": pct([s["epi_us"] for s in segs if s["k"] > 0]) if any(s["k"] > 0 for s in segs) else None,
-}
-print(json.dumps(res))
+print(json.dumps({"shape": shape, "layer_us_graph": round(ms * 1e3, 2)}))
 Path("gpurun_out").mkdir(exist_ok=True)
 np.save(f"gpurun_out/trace_{shape}.npy", buf)

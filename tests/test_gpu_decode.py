@@ -552,6 +552,46 @@ def test_decode_launch_count_policy():
     assert lib.pqb_decode_launches(8, 1, 4096, 0) == 1  # LUT kernel: merge in-kernel
 
 
+@pytest.mark.parametrize("G", [4, 8])
+@pytest.mark.parametrize("values", ["bf16", "f32", "vq4"])
+def test_dq_split_shapes(G, values):
+    """The DQ kernel's persistent work split (decode_dq.cu): ragged units cut at
+    CTA counts from one CTA to a few tiles per CTA, so CTA ranges start and end
+    inside units, cover several whole units and run past a unit's last tile
+    (many merge segments per unit).  Outputs within
+    the fp32 tolerance of softmax64(exact scores) . V at every split, the
+    separate merge launch bit-identical to the in-kernel merge, and the fast
+    shared-memory layout in use."""
+    lens = [1, 33, 700, 64, 2000, 5, 129, 1024]
+    U, T, res = len(lens), max(lens), 8
+    rng = np.random.default_rng(G * 7 + len(values))
+    keys = [po.synthetic_keys(t, 128, seed=1300 + u, outliers=(0, 1)) for u, t in enumerate(lens)]
+    vals = [rng.standard_normal((t, 128)).astype(np.float32) for t in lens]
+    q = rng.standard_normal((U, G, 128)).astype(np.float32)
+    vkw = dict(value_bits=4) if values == "vq4" else dict(value_dtype=torch.float32 if values == "f32" else torch.bfloat16)
+    cache = pq.PolarKVCache(pq.QuantConfig(4, 4), U, 128, res, capacity=T + 1, page_tokens=64, **vkw)
+    for u in range(U):
+        cache.prefill(torch.from_numpy(keys[u]).cuda().unsqueeze(0), torch.from_numpy(vals[u]).cuda().unsqueeze(0),
+                      unit_start=u)
+    refs = []
+    for u in range(U):
+        a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
+        s16 = cache.scales16[u].cpu().numpy()
+        vv = cache.values_f32(u).cpu().numpy().astype(np.float64)
+        resid = keys[u][lens[u] - min(res, lens[u]):]
+        refs.append([po.softmax64(po.lut_scores(q[u, g], a, r, s16, 4, 4, 1, resid), 1.0 / math.sqrt(128)) @ vv
+                     for g in range(G)])
+    qd = torch.from_numpy(q).cuda()
+    for splits in (1, 2, 3, 5, 13, 40, 148):
+        out = cache.decode(qd, splits=splits).cpu().numpy()
+        sep = cache.decode(qd, splits=splits, flags=pq._lib.PQB_DECODE_MERGE_KERNEL).cpu().numpy()
+        assert np.array_equal(out, sep), splits
+        for u in range(U):
+            for g in range(G):
+                peak_close(out[u, g], refs[u][g], OUT_RTOL_F32)
+    assert pq._lib.load().pqb_decode_dq_layout() == 1  # the product table at its fixed address
+
+
 @pytest.mark.parametrize("m,n", [(4, 4), (3, 2), (2, 4), (3, 4)])
 @pytest.mark.parametrize("G", [4, 8])
 @pytest.mark.parametrize("lay,res,page", [(1, 0, 256), (0, 40, 64), (1, 16, 32)])
