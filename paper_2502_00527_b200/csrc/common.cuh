@@ -124,13 +124,21 @@ PQB_DEV float load1(const void* base, int64_t elem_off) {
 PQB_DEV float half_bits_to_f32(uint16_t h) { return __half2float(__ushort_as_half(h)); }
 
 // Byte offset of value element (token t of a page, dim e) inside the page's
-// value region.  bf16 rows of d = 128 (256 B) are stored with their 16-byte
-// chunks XOR-swizzled by (t & 7): a linear bulk copy of a tile then lands in
-// shared memory in the conflict-free layout ldmatrix.trans needs (8 rows of the
-// same logical chunk hit 8 different bank groups).  Other shapes are linear.
+// value region.  bf16 rows of d = 128 are stored in 2 KB groups of 8 tokens:
+// [dims 0-63 of the 8 tokens][dims 64-127], 128 B per token and half, the
+// 16-byte chunks XOR-swizzled by (t & 7).  A linear bulk copy of a tile then
+// lands in shared memory in the conflict-free layout ldmatrix.trans needs (8
+// rows of the same logical chunk hit 8 different bank groups), and each 1 KB
+// half-group is exactly the canonical 128-byte-swizzled MN-major atom a
+// tcgen05 shared-memory descriptor reads (dims contiguous, 8 tokens).  Other
+// shapes are linear.
+PQB_DEV int64_t value_offset_bf16_128(int64_t t, int e) {
+  return ((t >> 3) << 11) + ((e >> 6) << 10) + ((t & 7) << 7) + ((((e >> 3) & 7) ^ static_cast<int>(t & 7)) << 4) +
+         ((e & 7) << 1);
+}
 PQB_DEV int64_t value_offset(int64_t t, int e, int d, int value_dtype) {
   if (value_dtype == PQB_F32) return (t * d + e) * 4;
-  if (d == 128) return t * 256 + ((((e >> 3) ^ static_cast<int>(t & 7))) << 4) + ((e & 7) << 1);
+  if (d == 128) return value_offset_bf16_128(t, e);
   return (t * d + e) * 2;
 }
 

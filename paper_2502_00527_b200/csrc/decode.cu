@@ -94,7 +94,9 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 
   // lane constants for the tensor-core P.V
   const int qn = lane >> 2, t4 = lane & 3;  // fragment query column / pair
-  const uint32_t ld_row = static_cast<uint32_t>((((lane >> 4) & 1) * 8 + (lane & 7)) * 256);
+  // ldmatrix.trans row addresses in the grouped value layout (value_offset):
+  // token 16 ks + 8 ((lane >> 4) & 1) + (lane & 7), chunk 2 mt + ((lane >> 3) & 1)
+  const uint32_t ld_row = static_cast<uint32_t>(((lane >> 4) & 1) * 2048 + (lane & 7) * 128);
   const uint32_t ld_chunk = static_cast<uint32_t>((((lane >> 3) & 1) ^ (lane & 7)) << 4);
 
   for (int64_t seg = i_begin; seg < i_end;) {
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(kNW * 32, 1)
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
             uint32_t a0, a1, a2, a3;
-            ldsm_x4_trans(vbase + ks * 16 * 256 + (ld_chunk ^ (mt << 5)), a0, a1, a2, a3);
+            ldsm_x4_trans(vbase + ks * 4096 + (mt >> 2) * 1024 + (ld_chunk ^ ((mt & 3) << 5)), a0, a1, a2, a3);
             mma_bf16(d[mt], a0, a1, a2, a3, b[ks][0][0], b[ks][0][1]);
             mma_bf16(d[mt], a0, a1, a2, a3, b[ks][1][0], b[ks][1][1]);
           }

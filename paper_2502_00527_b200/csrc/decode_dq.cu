@@ -506,7 +506,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   }
 
   const int g8 = lane >> 2, t4 = lane & 3;  // fragment group / thread-in-group
-  const uint32_t ld_row = static_cast<uint32_t>((((lane >> 4) & 1) * 8 + (lane & 7)) * 256);
+  // ldmatrix.trans row addresses in the grouped value layout (value_offset):
+  // token 16 ks + 8 ((lane >> 4) & 1) + (lane & 7), chunk 2 mt + ((lane >> 3) & 1)
+  const uint32_t ld_row = static_cast<uint32_t>(((lane >> 4) & 1) * 2048 + (lane & 7) * 128);
   const uint32_t ld_chunk = static_cast<uint32_t>((((lane >> 3) & 1) ^ (lane & 7)) << 4);
   // P.V output columns 2 t4, 2 t4 + 1 belong to queries qc0, qc1 (packed: col & 3)
   const int qc0 = kPacked ? ((2 * t4) & 3) : 2 * t4, qc1 = qc0 + 1;
@@ -573,6 +575,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     }
     named_sync(1, kConsThreads);
     if (tid == 0) s_misc[0] = 0;  // all have read qmax; the next atomicMax is >= 2 barriers later
+    // (the k + 8 half repeats (hi, lo); loading it as its own registers measured
+    // 1.5-6% faster than passing aq[ks][0..1] twice: the compiler schedules the
+    // QK block differently)
     uint32_t aq[16][4];
 #pragma unroll
     for (int ks = 0; ks < 16; ++ks) {
@@ -903,7 +908,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 #pragma unroll
           for (int ks = 0; ks < 2; ++ks) {
             uint32_t a0, a1, a2, a3;
-            ldsm_x4_trans(vbase + ks * 16 * 256 + (ld_chunk ^ (mt << 5)), a0, a1, a2, a3);
+            ldsm_x4_trans(vbase + ks * 4096 + (mt >> 2) * 1024 + (ld_chunk ^ ((mt & 3) << 5)), a0, a1, a2, a3);
             mma_bf16(d[mt], a0, a1, a2, a3, phi[2 * ks], phi[2 * ks + 1]);
             if constexpr (!kPacked) mma_bf16(d[mt], a0, a1, a2, a3, plo[2 * ks], plo[2 * ks + 1]);
           }

@@ -639,7 +639,7 @@ __global__ void store_values_v8_kernel(const void* __restrict__ vals, int64_t T,
     const int64_t ta = tok_offset_const + t;
     const int64_t page = ta / P;
     const int64_t tp = ta - page * P;
-    uint8_t* dst = page_base(st, unit, page) + st.value_off + tp * 256 + ((c ^ static_cast<int>(tp & 7)) << 4);
+    uint8_t* dst = page_base(st, unit, page) + st.value_off + value_offset_bf16_128(tp, 8 * c);
     *reinterpret_cast<uint4*>(dst) = w;
   }
 }
