@@ -123,6 +123,25 @@ struct DqCfg {
   static_assert(kNW * kSt * kStageBytes >= kNW * G * 132 * 4, "merge area");
 };
 
+// PQB_DQ_UMMA=1 (A/B build): P.V of the G = 4 bf16-value kernel on the 5th-
+// generation tensor cores instead of mma.sync.  The four compute warps of a
+// warpgroup score their tiles as before and share one online-softmax reference
+// max (exchanged through shared memory, raised lazily: only when a tile max
+// exceeds it by more than 2^8, so P <= 256); each warp writes its P^T (bf16 hi
+// | lo columns) as K-major core matrices, and one elected thread issues
+//   O^T[128 dims x 8] += V^T[128 x 128 tokens] . P^T[128 x 8]
+// as 8 tcgen05.mma (M 128, N 8, K 16) straight from the warps' TMA-filled value
+// stages (the grouped value layout is the 128-byte-swizzled MN-major
+// canonical form), accumulating in tensor memory.  A stage is released once
+// the MMAs reading it commit (next round); O is read back with tcgen05.ld at
+// the end of the segment and rescaled there when the reference max rises.
+#ifndef PQB_DQ_UMMA
+#define PQB_DQ_UMMA 0
+#endif
+constexpr int kGapUmmaB = 164;    // 64 slots: P^T core matrices [wg][parity][warp][chunk]
+constexpr int kGapUmmaMisc = 228;  // tile maxes, row sums, stage addresses, mbarriers, TMEM base
+constexpr float kUmmaTau = 8.0f;   // lazy max: rescale only when a tile max exceeds the reference by > 2^8
+
 // PQB_DQ_TRACE=1 (probe builds only): consumer thread 0 of every CTA stamps
 // %globaltimer at the launch phases into pqb_dq_trace[cta][32] (read back by
 // pqb_debug_dq_trace; scripts/trace_probe.py): [0] entry, [1] after the grid
@@ -365,13 +384,17 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   constexpr bool kScores = PROBE == kDqScores;
   constexpr bool kFused = M == 4 && N == 4;
   constexpr bool kPacked = Cfg::kPacked;
+  // (m = n = 4: the codes take 2 KB of the 10 KB stage, so value tiles stay 1 KB aligned)
+  constexpr bool kUmma = PQB_DQ_UMMA && PQB_DQ_PRMT_TAB && VQ == kValBf16 && G == 4 && M == 4 && N == 4 && PROBE == 0;
   static_assert(G == 1 || G == 2 || G == 4 || G == 8, "G");
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   DQ_TRACE(tid == 0, 0);
 #if PQB_DQ_PRMT_TAB
   const int tab_off = static_cast<int>(kPtTabAbs - smem_u32(smem));  // dynamic offset of the table
-  const int n_before = tab_off / Cfg::kStageBytes;                     // stages before the table
+  // UMMA: value tiles 1 KB aligned (the 128-byte swizzle pattern is taken from address bits 7-9)
+  const int st_pad = kUmma ? static_cast<int>((1024u - (smem_u32(smem) & 1023u)) & 1023u) : 0;
+  const int n_before = (tab_off - st_pad) / Cfg::kStageBytes;          // stages before the table
   uint8_t* const tabp = smem + tab_off;
   uint2* ptab = reinterpret_cast<uint2*>(tabp);  // entry e at slot e (e * 32 uint2)
   const GapArr<uint4> qfrag{tabp, kGapQfrag};
@@ -380,14 +403,26 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   float2* cs_s = reinterpret_cast<float2*>(tabp + kGapCs * 256 + 128);
   const GapArr<float> s_scale{tabp, kGapScale};  // 64 floats: two gaps
   auto stage_ptr = [&](int i) -> uint8_t* {
-    return smem + (i < n_before ? i * Cfg::kStageBytes : tab_off + 65536 + (i - n_before) * Cfg::kStageBytes);
+    return smem + (i < n_before ? st_pad + i * Cfg::kStageBytes : tab_off + 65536 + (i - n_before) * Cfg::kStageBytes);
   };
   uint8_t* warp_area = smem;  // merge scratch aliases the first stages (all before the table)
   if (tid == 0 && (tab_off < 0 || n_before * Cfg::kStageBytes < kNW * G * 132 * 4 ||
                    tab_off + 65536 + (kNW * kSt - n_before) * Cfg::kStageBytes > Cfg::kSmem))
     __trap();  // shared-window layout other than measured: the table cannot sit at kPtTabAbs
   const GapArr<float> rbuf{tabp, kGapRbuf + 8 * (warp < kNW ? warp : 0)};
+  uint8_t* const um_b = tabp + kGapUmmaB * 256 + 128;      // P^T core matrix k at um_b + 256 k
+  float* const um_max = reinterpret_cast<float*>(tabp + kGapUmmaMisc * 256 + 128);        // [2][4][4]
+  float* const um_l = reinterpret_cast<float*>(tabp + (kGapUmmaMisc + 1) * 256 + 128);    // [2][4][4]
+  uint32_t* const um_va = reinterpret_cast<uint32_t*>(tabp + (kGapUmmaMisc + 2) * 256 + 128);  // [2][4]
+  uint64_t* const um_bar = reinterpret_cast<uint64_t*>(um_va + 8);                              // [2][2]
+  uint32_t* const um_tmem = reinterpret_cast<uint32_t*>(um_bar + 4);
 #else
+  uint8_t* const um_b = smem;  // (the UMMA variant needs the PRMT layout's gap slots)
+  float* const um_max = nullptr;
+  float* const um_l = nullptr;
+  uint32_t* const um_va = nullptr;
+  uint64_t* const um_bar = nullptr;
+  uint32_t* const um_tmem = nullptr;
   uint2* ptab = reinterpret_cast<uint2*>(smem);                                   // [2^(M+N)][16]
   uint4* qfrag = reinterpret_cast<uint4*>(smem + Cfg::kTabBytes);                    // [16][32]
   float* q_s = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(qfrag) + Cfg::kFragBytes);  // [G][128]
@@ -417,6 +452,19 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     }
     fence_mbar_init();
   }
+  if constexpr (kUmma) {  // MMA-completion barriers and 32 columns of tensor memory (2 x 8 used)
+    if (tid == 0) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mbar_init(um_bar + k, 1);
+      fence_mbar_init();
+    }
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(um_tmem))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+  }
   // product table (once per CTA): PT[(a << N) | r][copy] = (r cos_a, r sin_a) as fp16 hi + lo
   if (tid == 0) s_misc[0] = 0;
   if (tid < (1 << M)) {
@@ -439,6 +487,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     for (int k = 0; k < 8; ++k) dst[k] = make_uint4(hi, lo, hi, lo);
   }
   if constexpr (kDqWs) __syncthreads();  // producers helped build the table
+  uint32_t tmem_base = 0;
+  if constexpr (kUmma) {
+    tc_fence_after();
+    tmem_base = *um_tmem;
+  }
+  uint32_t u_round = 0;  // UMMA: this warpgroup's P.V rounds so far (mbarrier phases)
 #if PQB_DQ_PRMT_TAB
   const uint32_t ptab_l = kPtTabAbs | ((lane & 15) << 3);  // this lane's bank-slot copy
 #else
@@ -593,56 +647,9 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     if (tid == 0 && n_seg_tr < 6) pqb_dq_trace[blockIdx.x * 32 + 5 + 4 * n_seg_tr] = unit;
 #endif
 
-    // ---- lane 0 fills this warp's ring with its first tiles
-    TileCursor cur;
-    cur.init(first, tpp);
-    if (!kDqWs && lane == 0) {
-#pragma unroll
-      for (int s = 0; s < kSt; ++s) {
-        if (cur.tile < t_hi) {
-          fence_proxy_async_smem();
-          const uint32_t sl = (k_iter + s) % kSt;
-          issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kSt + sl), c.store,
-                                  page_base_c(c.store, unit, PROBE == 2 ? 0 : cur.pg), PROBE == 2 ? 0 : cur.tin,
-                                  bar + sl);
-        }
-        cur.next(dpg, dtin, tpp);
-      }
-    }
-    float m_run = -INFINITY, l_run = 0.0f;  // query g8 (lanes g8 < G)
-    float z_run = 0.0f;                     // VQ: sum_t p_t zp_t of query g8 (lane partial)
-    float d[8][4];
-#pragma unroll
-    for (int mt = 0; mt < 8; ++mt)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) d[mt][k] = 0.0f;
-    float o[G][4];  // fp32 values: output dims 4 lane .. 4 lane + 3 of every query
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-#pragma unroll
-      for (int k = 0; k < 4; ++k) o[g][k] = 0.0f;
-
-    for (int tile = first; tile < t_hi; tile += kNW, ++k_iter) {
-      const uint32_t s = k_iter % kSt;
-      const int nt = tile + kSt * kNW;  // the tile this stage is refilled with
-      mbar_wait(bar + s, (k_iter / kSt) & 1);
-      const uint8_t* st = stage_ptr(warp * kSt + s);
-      const int tok0 = tile * kTile;
-      if constexpr (PROBE == 1) {
-        __syncwarp();
-        if (kDqWs) {
-          if (lane == 0) mbar_arrive(&s_empty[warp][s]);
-        } else if (lane == 0) {
-          if (nt < t_hi) {
-            fence_proxy_async_smem();
-            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kSt + s), c.store, page_base_c(c.store, unit, cur.pg), cur.tin,
-                                    bar + s);
-          }
-          cur.next(dpg, dtin, tpp);
-        }
-        continue;
-      }
-
+    // S = Q' . K^T of one tile (+ the residual window's exact dots): lane (g8, t4)
+    // gets query g8 at tokens 8 nb + 2 t4 + j in x[nb][j], unscaled
+    auto tile_scores = [&](const uint8_t* st, int tok0, float (&x)[4][2]) {
       // ---- S = Q' . K^T on the tensor cores: n-block nb = tokens 8 nb .. 8 nb + 7;
       // this lane gathers the keys of token 8 nb + g8 (B column g8).
       float sc[4][4];
@@ -681,7 +688,6 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         }
       }
       // lane (g8, t4): query g8, tokens 8 nb + 2 t4 + j  (hi row + lo row)
-      float x[4][2];
 #pragma unroll
       for (int nb = 0; nb < 4; ++nb) {
         x[nb][0] = sc[nb][0] + sc[nb][2];
@@ -713,6 +719,204 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           }
         __syncwarp();
       }
+    };
+
+    // ---- lane 0 fills this warp's ring with its first tiles
+    TileCursor cur;
+    cur.init(first, tpp);
+    if (!kDqWs && lane == 0) {
+#pragma unroll
+      for (int s = 0; s < kSt; ++s) {
+        if (cur.tile < t_hi) {
+          fence_proxy_async_smem();
+          const uint32_t sl = (k_iter + s) % kSt;
+          issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kSt + sl), c.store,
+                                  page_base_c(c.store, unit, PROBE == 2 ? 0 : cur.pg), PROBE == 2 ? 0 : cur.tin,
+                                  bar + sl);
+        }
+        cur.next(dpg, dtin, tpp);
+      }
+    }
+    float m_run = -INFINITY, l_run = 0.0f;  // query g8 (lanes g8 < G)
+    float z_run = 0.0f;                     // VQ: sum_t p_t zp_t of query g8 (lane partial)
+    float d[8][4];
+#pragma unroll
+    for (int mt = 0; mt < 8; ++mt)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) d[mt][k] = 0.0f;
+    float o[G][4];  // fp32 values: output dims 4 lane .. 4 lane + 3 of every query
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) o[g][k] = 0.0f;
+
+    if constexpr (kUmma) {
+      // ---- P.V on tcgen05, warpgroup-synchronous rounds (PQB_DQ_UMMA, see top)
+      const int wg = warp >> 2, wq = warp & 3;
+      const int t_wg = t_lo + 4 * wg;  // round k: warp wq of the group takes tile t_wg + wq + 8 k
+      const int n_rounds = t_hi > t_wg ? (t_hi - t_wg + 7) / 8 : 0;
+      const uint32_t tcol = tmem_base + 8 * wg;                    // D: lanes = dims, 8 columns
+      const uint32_t tq = tcol + (static_cast<uint32_t>(32 * wq) << 16);  // this warp's quarter of D
+      constexpr uint32_t kIdesc = umma_idesc_bf16(128, 8, 1);
+      int pend = -1;  // stage of this warp's previous tile, released once its MMAs commit
+      bool first_mma = true;
+      for (int k = 0; k < n_rounds; ++k, ++u_round) {
+        const int tile = t_wg + wq + 8 * k;
+        const bool has = tile < t_hi;
+        const int tok0 = tile * kTile;
+        uint32_t s = 0;
+        const uint8_t* st = nullptr;
+        float x[4][2];
+        if (has) {
+          s = k_iter % kSt;
+          mbar_wait(bar + s, (k_iter / kSt) & 1);
+          st = stage_ptr(warp * kSt + s);
+          tile_scores(st, tok0, x);
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            x[nb][j] = has && tok0 + 8 * nb + 2 * t4 + j < T ? x[nb][j] * xscale : -INFINITY;
+            mx = fmaxf(mx, x[nb][j]);
+          }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        if (t4 == 0 && g8 < G) um_max[(wg * 4 + wq) * 4 + g8] = mx;
+        named_sync(3 + wg, 128);
+        const int gq = g8 < G ? g8 : 0;
+        const float mt = fmaxf(fmaxf(um_max[(wg * 4 + 0) * 4 + gq], um_max[(wg * 4 + 1) * 4 + gq]),
+                               fmaxf(um_max[(wg * 4 + 2) * 4 + gq], um_max[(wg * 4 + 3) * 4 + gq]));
+        if (k > 0) {  // the previous round's MMAs: its stages and P^T buffer are free after this
+          mbar_wait(um_bar + wg * 2 + ((u_round - 1) & 1), ((u_round - 1) >> 1) & 1);
+          tc_fence_after();
+        }
+        if (pend >= 0) {
+          if (lane == 0) mbar_arrive(&s_empty[warp][pend]);
+          pend = -1;
+        }
+        // lazy reference max: raised only when the tile max exceeds it by more than 2^tau
+        const bool upd = g8 < G && mt > m_run + kUmmaTau;
+        const float m_new = upd ? mt : m_run;
+        const float alpha = upd ? fast_exp2(m_run - m_new) : 1.0f;
+        if (k > 0 && __any_sync(0xffffffffu, upd)) {  // rescale the accumulated O (columns q, q + 4: query q)
+          float v[8];
+          tmem_ld8(tq, v);
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) v[cc] *= __shfl_sync(0xffffffffu, alpha, (cc & 3) * 4);
+          tmem_st8(tq, v);
+        }
+        l_run *= alpha;
+        m_run = m_new;
+        float ls = 0.0f;
+        uint8_t* bbuf = um_b + ((wg * 2 + (u_round & 1)) * 16 + wq * 4) * 256;  // this warp's 4 core matrices
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+          const float p0 = fast_exp2(x[nb][0] - m_run), p1 = fast_exp2(x[nb][1] - m_run);
+          ls += p0 + p1;
+          const __nv_bfloat162 hi = __floats2bfloat162_rn(p0, p1);
+          const float2 hf = __bfloat1622float2(hi);
+          const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+          if (g8 < G) {  // core matrix nb (tokens 8 nb ..): row g8 = P_hi of query g8, row 4 + g8 = P_lo
+            *reinterpret_cast<__nv_bfloat162*>(bbuf + nb * 256 + g8 * 16 + t4 * 4) = hi;
+            *reinterpret_cast<__nv_bfloat162*>(bbuf + nb * 256 + (4 + g8) * 16 + t4 * 4) = lo;
+          }
+        }
+        l_run += ls;
+        fence_proxy_async_smem();  // P^T (generic stores) -> the tensor core's async proxy
+        if (lane == 0) um_va[wg * 4 + wq] = has ? smem_u32(st + Cfg::kABytes + Cfg::kRBytes) : 0u;
+        tc_fence_before();
+        named_sync(3 + wg, 128);
+        if (wq == 0 && lane == 0) {
+          tc_fence_after();
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const uint32_t va = um_va[wg * 4 + i];
+            if (va == 0u) continue;
+            const uint32_t bb = smem_u32(um_b + ((wg * 2 + (u_round & 1)) * 16 + i * 4) * 256);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              // A = V^T: MN-major, 128-byte swizzle, dims 64-127 at +1 KB, token groups at +2 KB;
+              // B = P^T: K-major core matrices, tokens 16 h + 8 .. at +256 B
+              umma_bf16(tcol, umma_smem_desc(va + h * 4096, 1024, 2048, 2), umma_smem_desc(bb + h * 512, 256, 256, 0),
+                        kIdesc, !first_mma);
+              first_mma = false;
+            }
+          }
+          umma_commit(um_bar + wg * 2 + (u_round & 1));
+        }
+        __syncwarp();
+        if (has) {
+          pend = static_cast<int>(s);
+          ++k_iter;
+        }
+      }
+      // ---- segment end: the last round's MMAs, then O^T back from tensor memory
+      float ov[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (n_rounds > 0) {
+        mbar_wait(um_bar + wg * 2 + ((u_round - 1) & 1), ((u_round - 1) >> 1) & 1);
+        tc_fence_after();
+        tmem_ld8(tq, ov);
+      }
+      if (pend >= 0 && lane == 0) mbar_arrive(&s_empty[warp][pend]);
+      l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+      l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+      if (t4 == 0 && g8 < G) um_l[(wg * 4 + wq) * 4 + g8] = l_run;
+      tc_fence_before();
+      named_sync(1, kConsThreads);  // every warp is past its last stage read and MMA
+      float* red = reinterpret_cast<float*>(warp_area);
+      // the group's partial goes in warp slot 4 wg (dims 32 wq + lane from each warp); slots
+      // 4 wg + 1 .. 3 stay empty (m = -inf)
+      float* grp = red + (4 * wg) * G * 132;
+#pragma unroll
+      for (int g = 0; g < G; ++g) grp[g * 132 + 4 + 32 * wq + lane] = ov[g] + ov[G + g];
+      const float mg = __shfl_sync(0xffffffffu, m_run, (lane & 3) * 4);  // query lane's reference max
+      if (lane < G) {
+        float* mine = red + warp * G * 132;
+        if (wq == 0) {
+          mine[lane * 132] = mg;
+          mine[lane * 132 + 1] = um_l[(wg * 4 + 0) * 4 + lane] + um_l[(wg * 4 + 1) * 4 + lane] +
+                                 um_l[(wg * 4 + 2) * 4 + lane] + um_l[(wg * 4 + 3) * 4 + lane];
+        } else {
+          mine[lane * 132] = -INFINITY;
+          mine[lane * 132 + 1] = 0.0f;
+        }
+      }
+      if (wq != 0) {  // the empty slots' accumulators must be finite (the merge weighs them by 0)
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+#pragma unroll
+          for (int k = 0; k < 4; ++k) red[(warp * G + g) * 132 + 4 + 32 * k + lane] = 0.0f;
+      }
+      finish_segment<G>(ep, ws, unit, red, s_misc + 1, tid, kConsThreads);
+      if constexpr (kDqWs) named_arrive(2, kDqThreads);  // producers may refill the stages
+      ++n_seg_tr;
+      continue;
+    }
+    for (int tile = first; tile < t_hi; tile += kNW, ++k_iter) {
+      const uint32_t s = k_iter % kSt;
+      const int nt = tile + kSt * kNW;  // the tile this stage is refilled with
+      mbar_wait(bar + s, (k_iter / kSt) & 1);
+      const uint8_t* st = stage_ptr(warp * kSt + s);
+      const int tok0 = tile * kTile;
+      if constexpr (PROBE == 1) {
+        __syncwarp();
+        if (kDqWs) {
+          if (lane == 0) mbar_arrive(&s_empty[warp][s]);
+        } else if (lane == 0) {
+          if (nt < t_hi) {
+            fence_proxy_async_smem();
+            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(warp * kSt + s), c.store, page_base_c(c.store, unit, cur.pg), cur.tin,
+                                    bar + s);
+          }
+          cur.next(dpg, dtin, tpp);
+        }
+        continue;
+      }
+
+      float x[4][2];
+      tile_scores(st, tok0, x);
       if constexpr (kScores) {  // raw scores: x = S * 2^e_sc (exact rescale), tokens 8 nb + 2 t4 + j
         if (g8 < G) {
           const float inv_sc = ldexpf(1.0f, -e_sc);
@@ -985,6 +1189,14 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     ++n_seg_tr;
   }
   peer_publish(ep, ep.counters + ws.items / ws.tiles_max, tid, kConsThreads);
+  if constexpr (kUmma) {
+    tc_fence_before();
+    named_sync(1, kConsThreads);
+    if (warp == 0) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem_base) : "memory");
+    }
+  }
   DQ_TRACE(tid == 0, 31);
 #if PQB_DQ_TRACE
   if (tid == 0) {
