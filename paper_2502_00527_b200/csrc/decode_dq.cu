@@ -140,7 +140,10 @@ struct DqCfg {
 #endif
 constexpr int kGapUmmaB = 164;    // 64 slots: P^T core matrices [wg][parity][warp][chunk]
 constexpr int kGapUmmaMisc = 228;  // tile maxes, row sums, stage addresses, mbarriers, TMEM base
-constexpr float kUmmaTau = 8.0f;   // lazy max: rescale only when a tile max exceeds the reference by > 2^8
+constexpr float kUmmaTau = 8.0f;
+#ifndef PQB_DQ_UMMA_RELEASE
+#define PQB_DQ_UMMA_RELEASE 1  // the issuing lane waits for the round's MMAs and releases the 4 stages at once
+#endif   // lazy max: rescale only when a tile max exceeds the reference by > 2^8
 
 // PQB_DQ_TRACE=1 (probe builds only): consumer thread 0 of every CTA stamps
 // %globaltimer at the launch phases into pqb_dq_trace[cta][32] (read back by
@@ -414,7 +417,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   float* const um_max = reinterpret_cast<float*>(tabp + kGapUmmaMisc * 256 + 128);        // [2][4][4]
   float* const um_l = reinterpret_cast<float*>(tabp + (kGapUmmaMisc + 1) * 256 + 128);    // [2][4][4]
   uint32_t* const um_va = reinterpret_cast<uint32_t*>(tabp + (kGapUmmaMisc + 2) * 256 + 128);  // [2][4]
-  uint64_t* const um_bar = reinterpret_cast<uint64_t*>(um_va + 8);                              // [2][2]
+  uint64_t* const um_bar = reinterpret_cast<uint64_t*>(um_va + 16);  // [2][2] (um_va: [2][4] addresses, [2][4] stages)
   uint32_t* const um_tmem = reinterpret_cast<uint32_t*>(um_bar + 4);
 #else
   uint8_t* const um_b = smem;  // (the UMMA variant needs the PRMT layout's gap slots)
@@ -793,7 +796,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           tc_fence_after();
         }
         if (pend >= 0) {
-          if (lane == 0) mbar_arrive(&s_empty[warp][pend]);
+          if (!PQB_DQ_UMMA_RELEASE && lane == 0) mbar_arrive(&s_empty[warp][pend]);
           pend = -1;
         }
         // lazy reference max: raised only when the tile max exceeds it by more than 2^tau
@@ -825,7 +828,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         }
         l_run += ls;
         fence_proxy_async_smem();  // P^T (generic stores) -> the tensor core's async proxy
-        if (lane == 0) um_va[wg * 4 + wq] = has ? smem_u32(st + Cfg::kABytes + Cfg::kRBytes) : 0u;
+        if (lane == 0) {
+          um_va[wg * 4 + wq] = has ? smem_u32(st + Cfg::kABytes + Cfg::kRBytes) : 0u;
+          um_va[8 + wg * 4 + wq] = s;
+        }
         tc_fence_before();
         named_sync(3 + wg, 128);
         if (wq == 0 && lane == 0) {
@@ -845,6 +851,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             }
           }
           umma_commit(um_bar + wg * 2 + (u_round & 1));
+          if (PQB_DQ_UMMA_RELEASE) {  // the stages are free once the MMAs reading them are done
+            mbar_wait(um_bar + wg * 2 + (u_round & 1), (u_round >> 1) & 1);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (um_va[wg * 4 + i] != 0u) mbar_arrive(&s_empty[4 * wg + i][um_va[8 + wg * 4 + i]]);
+          }
         }
         __syncwarp();
         if (has) {
@@ -859,7 +871,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         tc_fence_after();
         tmem_ld8(tq, ov);
       }
-      if (pend >= 0 && lane == 0) mbar_arrive(&s_empty[warp][pend]);
+      if (!PQB_DQ_UMMA_RELEASE && pend >= 0 && lane == 0) mbar_arrive(&s_empty[warp][pend]);
       l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
       l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
       if (t4 == 0 && g8 < G) um_l[(wg * 4 + wq) * 4 + g8] = l_run;
