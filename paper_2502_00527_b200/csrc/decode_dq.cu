@@ -469,10 +469,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     tc_fence_before();
   }
   // product table (once per CTA): PT[(a << N) | r][copy] = (r cos_a, r sin_a) as fp16 hi + lo
-  if (tid == 0) {
-    s_misc[0] = 0;
-    s_misc[2] = 0;  // epilogue count (producers: the merge scratch is free)
-  }
+  if (tid == 0) s_misc[0] = 0;
   if (tid < (1 << M)) {
     float cf, sf;
     angle_unit(M, tid, cf, sf);
@@ -524,46 +521,30 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PQB_DQ_PROD_REGS) : "memory");
       const int w0 = warp - kNW, w1 = w0 + 4;
       uint32_t it0 = 0, it1 = 0;
-      // The end-of-segment merge scratch (red) aliases the first stages (warp 0's
-      // ring at G = 4, warps 0-1 at G = 8).  Only tiles bound for those stages
-      // wait until the consumers are past the previous segment's merge (the
-      // epilogue count in s_misc[2]); every other ring is refilled during the
-      // merge and the next unit's setup.
-      const uint8_t* red_end = warp_area + (kScores ? 0 : kNW * G * 132 * 4);
-      int seg_i = 0;
-      for (int64_t seg = i_begin; seg < i_end; ++seg_i) {
+      bool first_seg = true;
+      for (int64_t seg = i_begin; seg < i_end;) {
         const int64_t unit = seg / ws.tiles_max;
         const int t_lo = static_cast<int>(seg - unit * ws.tiles_max);
         const int64_t seg_end = min(i_end, (unit + 1) * ws.tiles_max);
         seg = seg_end;
         const int n_tiles = (c.seq_lens[unit] + kTile - 1) / kTile;
         const int t_hi = min(static_cast<int>(seg_end - unit * ws.tiles_max), n_tiles);
+        // the previous segment's merge scratch aliases the stages
+        if (!first_seg) named_sync(2, kDqThreads);
+        first_seg = false;
         if (lane == 0) {
           TileCursor c0, c1;
           c0.init(t_lo + w0, tpp);
           c1.init(t_lo + w1, tpp);
-          bool epi_ok = seg_i == 0;
-          auto aliased = [&](int w, uint32_t it) { return stage_ptr(w * kSt + it % kSt) < red_end; };
           auto issue = [&](int w, uint32_t it, const TileCursor& cu) {
             const uint32_t s = it % kSt;
             // the ring starts empty: the first kSt fills need no release
             if (it >= kSt) mbar_wait(&s_empty[w][s], ((it / kSt) & 1) ^ 1);
-            if (!epi_ok && aliased(w, it)) {
-              int done;
-              do {
-                asm volatile("ld.acquire.cta.shared.b32 %0, [%1];" : "=r"(done) : "r"(smem_u32(s_misc + 2)) : "memory");
-              } while (done < seg_i && (__nanosleep(20), true));
-              epi_ok = true;
-            }
             fence_proxy_async_smem();
             issue_tile_dq<M, N, VQ, kScores>(stage_ptr(w * kSt + s), c.store,
                                     page_base_c(c.store, unit, PROBE == 2 ? 0 : cu.pg), PROBE == 2 ? 0 : cu.tin,
                                     &s_bar[w][s]);
           };
-          if (!epi_ok && c0.tile < t_hi && c1.tile < t_hi && aliased(w0, it0) && !aliased(w1, it1)) {
-            issue(w1, it1++, c1);  // warp w1's ring first: w0's waits for the merge
-            c1.next(dpg, dtin, tpp);
-          }
           while (c0.tile < t_hi) {  // c1 runs 4 tiles behind c0's stream position, never past it
             issue(w0, it0++, c0);
             c0.next(dpg, dtin, tpp);
@@ -575,6 +556,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         }
         __syncwarp();
       }
+      if (!first_seg) named_sync(2, kDqThreads);
       return;
     }
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(PQB_DQ_CONS_REGS) : "memory");
@@ -588,7 +570,6 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   // P.V output columns 2 t4, 2 t4 + 1 belong to queries qc0, qc1 (packed: col & 3)
   const int qc0 = kPacked ? ((2 * t4) & 3) : 2 * t4, qc1 = qc0 + 1;
 
-  int n_seg_c = 0;  // segments started (their merges finished: n_seg_c - 1)
   for (int64_t seg = i_begin; seg < i_end;) {
     const int64_t unit = seg / ws.tiles_max;
     const int t_lo = static_cast<int>(seg - unit * ws.tiles_max);
@@ -599,9 +580,6 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     const int t_hi = min(static_cast<int>(seg_end - unit * ws.tiles_max), n_tiles);
 
     named_sync(1, kConsThreads);  // previous segment is done with q_s / qfrag / merge area
-    if (tid == 0 && n_seg_c > 0)  // the previous segment's merge scratch is free again
-      asm volatile("st.release.cta.shared.b32 [%0], %1;" ::"r"(smem_u32(s_misc + 2)), "r"(n_seg_c) : "memory");
-    ++n_seg_c;
     const int first = t_lo + warp;
     // ---- unit setup: q rows, max |q * s|, then the Q' hi/lo A-fragments
     // one round of independent global loads: the G query rows and the 64 scales
@@ -924,6 +902,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           for (int k = 0; k < 4; ++k) red[(warp * G + g) * 132 + 4 + 32 * k + lane] = 0.0f;
       }
       finish_segment<G>(ep, ws, unit, red, s_misc + 1, tid, kConsThreads);
+      if constexpr (kDqWs) named_arrive(2, kDqThreads);  // producers may refill the stages
       ++n_seg_tr;
       continue;
     }
@@ -1166,7 +1145,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       }
     }
 
-    if constexpr (kScores) continue;  // scores-only: nothing to merge
+    if constexpr (kScores) {  // scores-only: nothing to merge
+      if constexpr (kDqWs) named_arrive(2, kDqThreads);
+      continue;
+    }
     // ---- segment epilogue: per-warp (m, l, o) -> shared, then the common merge
     DQ_TRACE(tid == 0 && n_seg_tr < 6, 3 + 4 * n_seg_tr);
     l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
@@ -1214,6 +1196,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       }
     }
     finish_segment<G>(ep, ws, unit, red, s_misc + 1, tid, kConsThreads);
+    if constexpr (kDqWs) named_arrive(2, kDqThreads);  // producers may refill the stages
     DQ_TRACE(tid == 0 && n_seg_tr < 6, 4 + 4 * n_seg_tr);
     ++n_seg_tr;
   }
