@@ -94,7 +94,13 @@ def build(force: bool = False, verbose_ptxas: bool = False, jobs: int | None = N
                     raise RuntimeError(f"nvcc failed on {src.name}:\n{out}")
                 if verbose_ptxas:
                     print(out)
-    if force or todo or not lib.exists() or any(o.stat().st_mtime > lib.stat().st_mtime for o in objs):
+    # relink when any object is new or the lib was linked from another object set
+    # (switching back to an older source version reuses its cached objects,
+    # which are older than the lib built in between)
+    stamp = lib.with_suffix(".so.objs")
+    obj_set = "\n".join(o.name for o in objs)
+    if (force or todo or not lib.exists() or not stamp.exists() or stamp.read_text() != obj_set
+            or any(o.stat().st_mtime > lib.stat().st_mtime for o in objs)):
         lib.parent.mkdir(parents=True, exist_ok=True)
         tmp = lib.with_suffix(".so.tmp")
         cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(tmp), *map(str, objs)]
@@ -102,6 +108,7 @@ def build(force: bool = False, verbose_ptxas: bool = False, jobs: int | None = N
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}{res.stderr}")
         os.replace(tmp, lib)
+        stamp.write_text(obj_set)
     if out is None:  # drop stale objects of older source versions
         keep = {o.name for o in objs}
         for o in BUILD.glob("*.o"):

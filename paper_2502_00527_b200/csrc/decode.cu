@@ -689,6 +689,7 @@ static bool use_dq(const DecodeArgs& a) {
 // equal or slightly slower.  PQB_DECODE_MERGE_KERNEL forces it.
 static bool separate_merge(int flags, int group, int max_tokens, const WorkSplit& ws) {
   const int64_t seg_max = (ws.tiles_max + ws.per_cta - 1) / ws.per_cta + 1;
+  if (flags & PQB_DECODE_MERGE_INKERNEL) return false;
   return (flags & PQB_DECODE_MERGE_KERNEL) || seg_max > 8 || (group == 8 && max_tokens >= 16384);
 }
 
