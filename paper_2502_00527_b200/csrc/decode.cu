@@ -31,6 +31,8 @@
 //   (atomic counter in the workspace) LSE-merges the partials -- one launch per
 //   decode call.
 #include "decode_common.cuh"
+
+#include <cstdlib>
 #include "kernels.h"
 
 #include <algorithm>
@@ -576,6 +578,8 @@ static int choose_splits(int64_t n_units, int max_tokens) {
 // fast kernel: persistent split over units x tiles
 static WorkSplit make_split(int64_t n_units, int max_tokens, int ctas) {
   WorkSplit w;
+  w.balanced = 0;
+  w.n_cta = 0;
   w.tiles_max = tiles_of(max_tokens);
   w.items = n_units * w.tiles_max;
   const int64_t c = std::max<int64_t>(1, std::min<int64_t>(ctas, w.items));
@@ -593,10 +597,67 @@ static WorkSplit make_split(int64_t n_units, int max_tokens, int ctas) {
 }
 
 static int fast_slots(int64_t n_units, int max_tokens) {
-  // CTAs touching one unit <= ceil(tiles_max / per_cta) + 1 with per_cta >= items / kMaxCtas
+  // CTAs touching one unit <= ceil(tiles_max / per_cta) + 1 with per_cta >= items / kMaxCtas;
+  // a balanced split's ranges are >= per_cta / 2 (make_split_balanced), hence 2x + 2
   const int tm = tiles_of(max_tokens);
   const int64_t per_min = std::max<int64_t>(1, (n_units * tm) / kMaxCtas);
-  return static_cast<int>(std::min<int64_t>(tm, (tm + per_min - 1) / per_min + 1));
+  return static_cast<int>(std::min<int64_t>(tm, 2 * ((tm + per_min - 1) / per_min) + 2));
+}
+
+// Segment cost in tiles for the DQ kernel's balanced split: a CTA range that
+// crosses into a second unit pays a second unit setup and a merge epilogue
+// (launch traces: ~4-8 us, i.e. ~20-35 tiles at one CTA's share of HBM), so it
+// gets that many fewer tiles and CTAs finish together.  PQB_SPLIT_COST
+// overrides (0: uniform ranges).
+static int split_cost() {
+  static const int c = [] {
+    const char* e = std::getenv("PQB_SPLIT_COST");
+    return e ? std::atoi(e) : 24;
+  }();
+  return c;
+}
+
+// Greedy balanced ranges: CTA ranges of budget B tiles, minus `cost` per unit
+// segment; a range that would cross a unit boundary with less than its second
+// segment's cost left stops at the boundary.  B is the smallest budget whose
+// greedy cover needs no more than `ctas` CTAs.  Uniform ranges are kept when
+// the cost is small against a CTA's share (short launches, many segments) or
+// the item space does not fit the table.
+static WorkSplit make_split_balanced(int64_t n_units, int max_tokens, int ctas) {
+  WorkSplit w = make_split(n_units, max_tokens, ctas);
+  const int cost = split_cost();
+  const int64_t tm = w.tiles_max, items = w.items;
+  if (cost <= 0 || ctas > kSplitMaxCtas || w.per_cta < 8 * cost || items >= (int64_t(1) << 31)) return w;
+  auto cover = [&](int64_t B, int32_t* starts) -> int {
+    int64_t s = 0;
+    int c = 0;
+    while (s < items && c <= ctas) {
+      if (starts && c < ctas) starts[c] = static_cast<int32_t>(s);
+      const int64_t bnd = (s / tm + 1) * tm;
+      int64_t e = s + (B - cost);
+      if (e > bnd) {
+        const int64_t e2 = s + (B - 2 * cost);
+        e = e2 > bnd ? e2 : bnd;
+      }
+      s = std::min(e, items);
+      ++c;
+    }
+    return c;
+  };
+  int64_t lo = w.per_cta / 2 + 2 * cost, hi = w.per_cta + 2 * cost;  // hi always covers in <= ctas
+  if (cover(lo, nullptr) <= ctas) hi = lo;
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) / 2;
+    if (cover(mid, nullptr) <= ctas) hi = mid;
+    else lo = mid;
+  }
+  const int n = cover(hi, w.starts);
+  if (n > ctas) return w;
+  w.starts[n] = static_cast<int32_t>(items);
+  w.n_cta = n;
+  w.balanced = 1;
+  w.per_cta = hi;
+  return w;
 }
 
 int decode_splits(int64_t n_units, int max_tokens) { return choose_splits(n_units, max_tokens); }
@@ -619,10 +680,10 @@ size_t decode_workspace_bytes(int64_t n_units, int group, int max_tokens, int d)
 }
 
 // Work split + epilogue arguments shared by the LUT and DQ fast kernels.
-static int fast_setup(const DecodeArgs& a, EpiArgs& ep, WorkSplit& ws, int& grid) {
+static int fast_setup(const DecodeArgs& a, EpiArgs& ep, WorkSplit& ws, int& grid, bool balanced = false) {
   const int ctas = a.splits > 0 ? std::min(a.splits, kMaxCtas) : std::min(num_sms(), kMaxCtas);
-  ws = make_split(a.n_units, a.max_tokens, ctas);
-  grid = static_cast<int>((ws.items + ws.per_cta - 1) / ws.per_cta);
+  ws = balanced ? make_split_balanced(a.n_units, a.max_tokens, ctas) : make_split(a.n_units, a.max_tokens, ctas);
+  grid = ws.balanced ? ws.n_cta : static_cast<int>((ws.items + ws.per_cta - 1) / ws.per_cta);
   ep.out = a.out;
   ep.out_dtype = a.out_dtype;
   ep.slots = fast_slots(a.n_units, a.max_tokens);
@@ -695,7 +756,7 @@ static bool separate_merge(int flags, int group, int max_tokens, const WorkSplit
 
 int decode_launch_count(int64_t n_units, int group, int max_tokens, int flags) {
   if (group != 4 && group != 8) return 1;
-  const WorkSplit ws = make_split(n_units, max_tokens, std::min(num_sms(), kMaxCtas));
+  const WorkSplit ws = make_split_balanced(n_units, max_tokens, std::min(num_sms(), kMaxCtas));
   return (flags & PQB_DECODE_NO_COMBINE) || !separate_merge(flags, group, max_tokens, ws) ? 1 : 2;
 }
 
@@ -706,7 +767,7 @@ static int launch_dq_path(const DecodeArgs& a, cudaStream_t s, bool& handled) {
   EpiArgs ep;
   WorkSplit ws;
   int grid = 0;
-  const int rc = fast_setup(a, ep, ws, grid);
+  const int rc = fast_setup(a, ep, ws, grid, true);
   if (rc != PQB_OK) {
     handled = true;
     return rc;

@@ -240,13 +240,35 @@ PQB_DEV void peer_publish(const EpiArgs& ep, int* grid_done, int tid, int nthrea
 // Persistent work split: items = n_units * tiles_max, CTA c owns
 // [c*per_cta, min(items, (c+1)*per_cta)).  The slot of (unit u, CTA c) is
 // c - first_cta(u).
+// Cost-balanced split (DQ kernel, host make_split_balanced): CTA c owns
+// [starts[c], starts[c + 1]); a CTA whose range crosses into a second unit is
+// given fewer tiles (each unit segment costs a setup and a merge epilogue).
+constexpr int kSplitMaxCtas = 256;
 struct WorkSplit {
   int64_t items, per_cta;
   int tiles_max;
+  int balanced;  // 0: uniform per_cta ranges
+  int n_cta;     // CTAs of the decode launch (balanced)
+  int32_t starts[kSplitMaxCtas + 1];
 };
 
-PQB_DEV int64_t first_cta(const WorkSplit& w, int64_t unit) { return (unit * w.tiles_max) / w.per_cta; }
-PQB_DEV int64_t last_cta(const WorkSplit& w, int64_t unit) { return ((unit + 1) * w.tiles_max - 1) / w.per_cta; }
+PQB_DEV int64_t cta_begin(const WorkSplit& w, int64_t c) { return w.balanced ? w.starts[c] : c * w.per_cta; }
+PQB_DEV int64_t cta_end(const WorkSplit& w, int64_t c) {
+  return w.balanced ? w.starts[c + 1] : min(w.items, (c + 1) * w.per_cta);
+}
+// the CTA whose range holds item i (balanced: the last c with starts[c] <= i)
+PQB_DEV int64_t cta_of(const WorkSplit& w, int64_t i) {
+  if (!w.balanced) return i / w.per_cta;
+  int lo = 0, hi = w.n_cta;  // invariant: starts[lo] <= i < starts[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (w.starts[mid] <= i) lo = mid;
+    else hi = mid;
+  }
+  return lo;
+}
+PQB_DEV int64_t first_cta(const WorkSplit& w, int64_t unit) { return cta_of(w, unit * w.tiles_max); }
+PQB_DEV int64_t last_cta(const WorkSplit& w, int64_t unit) { return cta_of(w, (unit + 1) * w.tiles_max - 1); }
 
 // LSE merge of a unit's segment partials: out = sum_s O_s 2^(m_s - M) / sum_s l_s 2^(m_s - M).
 // It runs in the tail of the launch (the last CTA of a unit), so its L2 reads

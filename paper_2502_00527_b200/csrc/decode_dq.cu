@@ -510,8 +510,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   DQ_TRACE(tid == 0, 1);
   const int tpp = c.store.page_tokens / kTile;  // tiles per page
   const int dpg = kNW / tpp, dtin = kNW - (kNW / tpp) * tpp;  // cursor step of kNW tiles
-  const int64_t i_begin = static_cast<int64_t>(blockIdx.x) * ws.per_cta;
-  const int64_t i_end = min(ws.items, i_begin + ws.per_cta);
+  const int64_t i_begin = cta_begin(ws, blockIdx.x);
+  const int64_t i_end = cta_end(ws, blockIdx.x);
   uint32_t k_iter = 0;
   int n_seg_tr = 0;  // PQB_DQ_TRACE: segment index
   (void)n_seg_tr;
