@@ -215,19 +215,25 @@ PQB_DEV void ef_angle2(float x0, float x1, float y0, float y1, float& worst, con
   c1 = tab[i1];
 }
 
-// rint(r / s) of two pairs (fast estimate, polar_math.cuh radius_raw_fast).
+// rint(r / s) of two pairs (fast estimate, polar_math.cuh radius_raw_fast),
+// returned biased: t = rq + 1.5 * 2^23 (the packer takes the code from t's low
+// mantissa bits).  q + 1.5 * 2^23 rounds q to the nearest integer, ties to
+// even, exactly as rintf for 0 <= q < 2^22; two packed adds replace two FRND
+// and the packer's per-code add.
 // Band: |q - rq| >= 0.5 - 2^-18 q, tested as dq^2 >= 0.25 - 2^-18 q (a
 // superset: (0.5 - e)^2 >= 0.25 - e), so worst_r collects dq^2 + 2^-18 q - 0.25.
-PQB_DEV void ef_radius2(F2 x, F2 y, F2 inv, float& rq0, float& rq1, float& worst_r, bool& rok) {
+constexpr float kRqBias = 12582912.0f;  // 1.5 * 2^23
+PQB_DEV void ef_radius2(F2 x, F2 y, F2 inv, float& t0, float& t1, float& worst_r, bool& rok) {
   const F2 r2 = ffma2(x, x, fmul2(y, y));
   rok &= in_safe_range_nonneg(r2.x) & in_safe_range_nonneg(r2.y);
   const F2 q = fmul2(fmul2(r2, F2{rsqrt_approx(r2.x), rsqrt_approx(r2.y)}), inv);
-  const F2 rq{rintf(q.x), rintf(q.y)};
+  const F2 t = fadd2(q, F2{kRqBias, kRqBias});               // rq + bias
+  const F2 rq = fadd2(t, F2{-kRqBias, -kRqBias});            // exact
   const F2 dq = ffma2(rq, F2{-1.0f, -1.0f}, q);  // exact
   const F2 m = ffma2(dq, dq, ffma2(q, F2{0x1p-18f, 0x1p-18f}, F2{-0.25f, -0.25f}));
   worst_r = fmaxf(worst_r, fmaxf(m.x, m.y));
-  rq0 = rq.x;
-  rq1 = rq.y;
+  t0 = t.x;
+  t1 = t.y;
 }
 
 // Does pair (x, y) sit in an ambiguity band (or outside the safe magnitude
@@ -278,11 +284,12 @@ struct EfArgs {
 };
 
 // Eight codes of B bits per lane of a token row -> the 32-bit chunk, with the
-// canonical forms applied.  Shared by the fast and the exact path.
+// canonical forms applied.  rt = radius codes biased by 1.5 * 2^23 (ef_radius2).
+// Shared by the fast and the exact path.
 template <int M, int N>
-PQB_DEV void ef_pack(const uint32_t (&ac)[8], const float (&rq)[8], uint32_t keep_a, uint32_t keep_r,
+PQB_DEV void ef_pack(const uint32_t (&ac)[8], const float (&rt)[8], uint32_t keep_a, uint32_t keep_r,
                      float& clamps, uint32_t& ca, uint32_t& cr) {
-  constexpr float kTop = static_cast<float>((1 << N) - 1);
+  constexpr float kTopB = kRqBias + static_cast<float>((1 << N) - 1);
   constexpr uint32_t kMagic = 0x4B400000u;  // bits of 1.5 * 2^23: f + 1.5*2^23 carries int(f) in the low bits
   // sum over the 8 fields of kMagic << (N * i), mod 2^32 (removed after packing)
   constexpr uint32_t kMagicSum = [] {
@@ -294,13 +301,13 @@ PQB_DEV void ef_pack(const uint32_t (&ac)[8], const float (&rq)[8], uint32_t kee
   cr = 0u;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    clamps += __saturatef(rq[i] - kTop);  // 1 iff rq >= top + 1 (integers)
-    const float rc = fminf(rq[i], kTop);
-    cr += __float_as_uint(rc + 12582912.0f) << (N * i);
+    clamps += __saturatef(rt[i] - kTopB);  // 1 iff rq >= top + 1 (integers)
+    const float rc = fminf(rt[i], kTopB);   // clamped code + bias (exact)
+    cr += __float_as_uint(rc) << (N * i);
     if constexpr (M == N) {
       ca += ac[i] << (M * i);
     } else {
-      const uint32_t a = rc == 0.0f ? (1u << (M - 1)) : ac[i];  // polar_codec.py:297
+      const uint32_t a = rc == kRqBias ? (1u << (M - 1)) : ac[i];  // polar_codec.py:297
       ca += a << (M * i);
     }
   }
@@ -495,7 +502,7 @@ __global__ void __launch_bounds__(kEfWarps * 32, 1) encode_fast_kernel(const EfA
           if (__any_sync(0xffffffffu, f)) {
             if (f && s32[i] > 0.0f) {
               bad |= !(fabsf(x[i]) <= 3.40282347e38f && fabsf(y[i]) <= 3.40282347e38f);
-              rq[i] = radius_raw_exact(x[i], y[i], s32[i]);
+              rq[i] = radius_raw_exact(x[i], y[i], s32[i]) + kRqBias;  // biased like ef_radius2
               ac[i] = angle_code_exact(x[i], y[i], M);
             }
           }
