@@ -592,6 +592,39 @@ def test_dq_split_shapes(G, values):
     assert pq._lib.load().pqb_decode_dq_layout() == 1  # the product table at its fixed address
 
 
+@pytest.mark.parametrize("G", [4, 8])
+def test_dq_balanced_split(G):
+    """The cost-balanced persistent split (CTA ranges of >= 192 tiles, so the
+    balancing is active: a range crossing into a second unit is shortened) at
+    several CTA counts: outputs within the fp32 tolerance of the oracle, and the
+    in-launch and separate-launch split merges bit-identical."""
+    lens = [20000, 13000, 20000, 7001, 16384]
+    U, T = len(lens), max(lens)
+    rng = np.random.default_rng(40 + G)
+    keys = [po.synthetic_keys(t, 128, seed=1700 + u, outliers=(0, 1)) for u, t in enumerate(lens)]
+    vals = [rng.standard_normal((t, 128)).astype(np.float32) for t in lens]
+    q = rng.standard_normal((U, G, 128)).astype(np.float32)
+    cache = pq.PolarKVCache(pq.QuantConfig(4, 4), U, 128, 0, capacity=T, page_tokens=256, value_dtype=torch.bfloat16)
+    for u in range(U):
+        cache.prefill(torch.from_numpy(keys[u]).cuda().unsqueeze(0), torch.from_numpy(vals[u]).cuda().unsqueeze(0),
+                      unit_start=u)
+    refs = []
+    for u in range(U):
+        a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
+        s16 = cache.scales16[u].cpu().numpy()
+        vb = torch.from_numpy(vals[u]).to(torch.bfloat16).float().numpy().astype(np.float64)
+        refs.append([po.softmax64(po.lut_scores(q[u, g], a, r, s16, 4, 4, 1), 1.0 / math.sqrt(128)) @ vb
+                     for g in range(G)])
+    qd = torch.from_numpy(q).cuda()
+    for splits in (3, 7, 11):
+        out = cache.decode(qd, splits=splits, flags=pq._lib.PQB_DECODE_MERGE_INKERNEL).cpu().numpy()
+        sep = cache.decode(qd, splits=splits, flags=pq._lib.PQB_DECODE_MERGE_KERNEL).cpu().numpy()
+        assert np.array_equal(out, sep), splits
+        for u in range(U):
+            for g in range(G):
+                peak_close(out[u, g], refs[u][g], OUT_RTOL_F32)
+
+
 @pytest.mark.parametrize("m,n", [(4, 4), (3, 2), (2, 4), (3, 4)])
 @pytest.mark.parametrize("G", [4, 8])
 @pytest.mark.parametrize("lay,res,page", [(1, 0, 256), (0, 40, 64), (1, 16, 32)])
