@@ -209,6 +209,7 @@ int pqb_decode_attn(const pqb_cache* cache, int64_t n_units, int group, const vo
 #define PQB_DECODE_MERGE_KERNEL 256 /* DQ fused call: split merge in a separate PDL launch instead of
                                        the last CTA of each unit (default for G = 8 from 16K tokens and
                                        when units are cut into more than 8 segments)                 */
+#define PQB_DECODE_NO_CLUSTER 2048 /* DQ fused call: no thread-block-cluster (DSMEM merge) path (A/B) */
 #define PQB_DECODE_MERGE_INKERNEL 1024 /* DQ fused call: last-CTA split merge inside the decode launch (A/B) */
 #define PQB_DECODE_DQ_LINEAR 512   /* DQ kernel: the linear shared-memory layout build (the automatic
                                        fallback when the default table placement does not fit)        */

@@ -23,6 +23,7 @@ PQB_VQ2, PQB_VQ8 = 17, 18  # 2- / 8-bit per-token value codes
 PQB_DECODE_FORCE_GENERIC, PQB_DECODE_NO_COMBINE, PQB_DECODE_DQ, PQB_DECODE_LUT = 1, 2, 4, 8
 PQB_DECODE_PROBE_MEM, PQB_DECODE_PROBE_COMPUTE = 64, 128
 PQB_DECODE_MERGE_KERNEL = 256
+PQB_DECODE_NO_CLUSTER = 2048  # DQ kernel: no cluster / DSMEM split-merge path (A/B)
 PQB_DECODE_MERGE_INKERNEL = 1024  # DQ kernel: force the in-launch split merge (A/B)
 PQB_DECODE_DQ_LINEAR = 512  # DQ kernel: linear shared-memory layout build (automatic fallback)
 

@@ -580,6 +580,7 @@ static WorkSplit make_split(int64_t n_units, int max_tokens, int ctas) {
   WorkSplit w;
   w.balanced = 0;
   w.n_cta = 0;
+  w.cluster = 0;
   w.tiles_max = tiles_of(max_tokens);
   w.items = n_units * w.tiles_max;
   const int64_t c = std::max<int64_t>(1, std::min<int64_t>(ctas, w.items));
@@ -754,8 +755,33 @@ static bool separate_merge(int flags, int group, int max_tokens, const WorkSplit
   return (flags & PQB_DECODE_MERGE_KERNEL) || seg_max > 8 || (group == 8 && max_tokens >= 16384);
 }
 
+// Thread-block-cluster path of the DQ kernel: when the units of a launch fill
+// the GPU with k = 2, 4 or 8 CTAs each (n_units * k >= 80 % of the SMs, no
+// more than the SMs), each unit is cut into k equal ranges run by one cluster,
+// and the split merge goes through distributed shared memory (finish_cluster):
+// no CTA straddles two units, no partials in global memory, no merge launch.
+// configs[3] (32 units of G = 8): k = 4.  0 when the call or the device
+// (resident clusters) does not qualify.
+static int dq_cluster_size(int64_t n_units, int group, int max_tokens, int flags, const pqb_cache* c,
+                           bool peer, bool scores) {
+  if ((group != 4 && group != 8) || peer || scores) return 0;
+  if (flags & (PQB_DECODE_MERGE_KERNEL | PQB_DECODE_MERGE_INKERNEL | PQB_DECODE_NO_CLUSTER |
+               PQB_DECODE_LUT | PQB_DECODE_DQ_LINEAR | PQB_DECODE_PROBE_MEM | PQB_DECODE_PROBE_COMPUTE))
+    return 0;
+  if (c != nullptr && (c->angle_bits != 4 || c->radius_bits != 4 || c->store.value_dtype != PQB_BF16)) return 0;
+  const int sms = num_sms(), tm = tiles_of(max_tokens);
+  for (int k : {8, 4, 2}) {
+    if (n_units * k > sms || n_units * k * 5 < static_cast<int64_t>(sms) * 4 || tm % k != 0 || tm / k < 64) continue;
+    if (dq_prmt::dq_cluster_capacity(group, 44, PQB_BF16, k) < n_units) return 0;
+    return k;
+  }
+  return 0;
+}
+
 int decode_launch_count(int64_t n_units, int group, int max_tokens, int flags) {
   if (group != 4 && group != 8) return 1;
+  // (the cluster path needs m = n = 4 with bf16 values; the count assumes that store)
+  if (dq_cluster_size(n_units, group, max_tokens, flags, nullptr, false, false) > 1) return 1;
   const WorkSplit ws = make_split_balanced(n_units, max_tokens, std::min(num_sms(), kMaxCtas));
   return (flags & PQB_DECODE_NO_COMBINE) || !separate_merge(flags, group, max_tokens, ws) ? 1 : 2;
 }
@@ -767,10 +793,28 @@ static int launch_dq_path(const DecodeArgs& a, cudaStream_t s, bool& handled) {
   EpiArgs ep;
   WorkSplit ws;
   int grid = 0;
+  const int cl = a.splits > 0 || a.out == nullptr
+                     ? 0
+                     : dq_cluster_size(a.n_units, a.group, a.max_tokens, a.flags, a.cache, a.peer != nullptr,
+                                       a.scores != nullptr);
   const int rc = fast_setup(a, ep, ws, grid, true);
   if (rc != PQB_OK) {
     handled = true;
     return rc;
+  }
+  if (cl > 1) {  // aligned split: cluster u = unit u, CTA rank r = tiles [r tm / k, (r + 1) tm / k)
+    ws.balanced = 0;
+    ws.cluster = cl;
+    ws.per_cta = ws.tiles_max / cl;
+    grid = static_cast<int>(a.n_units * cl);
+    ep.merge = !(a.flags & PQB_DECODE_NO_COMBINE);  // NO_COMBINE: the CTA partials only (kernel-only timing)
+    const int rc2 = dq_prmt::launch_decode_dq(a, ep, ws, grid, s, handled);
+    if (rc2 == PQB_OK && handled) g_dq_layout.store(1, std::memory_order_relaxed);
+    if (rc2 != kDqLayoutUnavailable) return rc2;
+    ws.cluster = 0;  // (the layout check failed: the non-cluster path below)
+    DecodeArgs b = a;
+    b.flags |= PQB_DECODE_NO_CLUSTER;
+    return launch_dq_path(b, s, handled);
   }
   const bool sep = ep.merge && a.out != nullptr && a.peer == nullptr &&
                    separate_merge(a.flags, a.group, a.max_tokens, ws);

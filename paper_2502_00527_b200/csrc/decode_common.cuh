@@ -249,6 +249,7 @@ struct WorkSplit {
   int tiles_max;
   int balanced;  // 0: uniform per_cta ranges
   int n_cta;     // CTAs of the decode launch (balanced)
+  int cluster;   // DQ: CTAs per thread-block cluster (> 1: aligned split, merge through DSMEM)
   int32_t starts[kSplitMaxCtas + 1];
 };
 
@@ -372,10 +373,12 @@ constexpr int kDqLayoutUnavailable = -1;
 namespace dq_prmt {
 int launch_decode_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s,
                      bool& handled);
+int dq_cluster_capacity(int group, int mn, int value_dtype, int cl);
 }
 namespace dq_lin {
 int launch_decode_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s,
                      bool& handled);
+int dq_cluster_capacity(int group, int mn, int value_dtype, int cl);
 }
 
 }  // namespace pqb

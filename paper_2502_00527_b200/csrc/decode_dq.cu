@@ -375,7 +375,93 @@ struct TileCursor {
   }
 };
 
-template <int G, int M, int N, int PROBE = 0, int VQ = 0>
+// ---- thread-block cluster: the split merge of a unit's K CTAs through
+// distributed shared memory (decode_dq_kernel CL > 1).
+PQB_DEV void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+PQB_DEV uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+PQB_DEV float ld_dsmem(const float* local, uint32_t rank) {  // the same smem offset in CTA `rank` of the cluster
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(local)), "r"(rank));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
+}
+
+// End of the single segment of a cluster CTA (aligned split: the K CTAs of a
+// cluster cut one unit into K equal ranges).  The CTA merges its warps into
+// cpart[g][130] (m, l, o[128]; the arithmetic of finish_segment), then, after
+// a cluster barrier, CTA rank r LSE-merges the K partials of dims
+// [r 128 / K, (r + 1) 128 / K) read from its peers' shared memory, in rank
+// order (merge_slots' arithmetic: outputs bit-identical to the global-slot
+// merge of the same split), and stores the output.  No partials in global
+// memory, no counter, no merge launch.  A second cluster barrier keeps every
+// CTA's partial alive until its peers have read it.  Callers: all consumer
+// threads (the producers only join the two cluster barriers).
+template <int G, int K>
+PQB_DEV void finish_cluster(const EpiArgs& ep, int64_t unit, const float* red, float* cpart, int tid, int nthreads) {
+  static_assert(K >= 2 && K <= 8 && 128 % K == 0, "cluster size");
+  named_sync(1, nthreads);
+  for (int i = tid; i < G * 128; i += nthreads) {
+    const int g = i >> 7, e = i & 127;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kNW; ++w) mx = fmaxf(mx, red[(w * G + g) * 132]);
+    float L = 0.0f, O = 0.0f;
+    if (mx != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < kNW; ++w) {
+        const float* rw = red + (w * G + g) * 132;
+        const float sc = exp2f(rw[0] - mx);
+        L = fmaf(rw[1], sc, L);
+        O = fmaf(rw[4 + e], sc, O);
+      }
+    }
+    cpart[g * 130 + 2 + e] = O;
+    if (e == 0) {
+      cpart[g * 130] = mx;
+      cpart[g * 130 + 1] = L;
+    }
+  }
+  cluster_sync_all();
+  constexpr int kSlice = 128 / K;
+  const int e0 = static_cast<int>(cluster_rank()) * kSlice;
+  for (int i = tid; ep.merge && i < G * kSlice; i += nthreads) {  // (!merge: PQB_DECODE_NO_COMBINE timing)
+    const int g = i / kSlice, e = e0 + i % kSlice;
+    float ms[K], ls[K], os[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      ms[k] = ld_dsmem(cpart + g * 130, k);
+      ls[k] = ld_dsmem(cpart + g * 130 + 1, k);
+      os[k] = ld_dsmem(cpart + g * 130 + 2 + e, k);
+    }
+    float mx = -INFINITY, L = 0.0f, O = 0.0f;
+    float bm = mx;
+#pragma unroll
+    for (int k = 0; k < K; ++k) bm = fmaxf(bm, ms[k]);
+    if (bm != -INFINITY) {
+      const float r = exp2f(mx - bm);
+      L *= r;
+      O *= r;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        if (ms[k] == -INFINITY) continue;
+        const float sc = exp2f(ms[k] - bm);
+        L = fmaf(ls[k], sc, L);
+        O = fmaf(os[k], sc, O);
+      }
+    }
+    emit(ep, unit, g, e, O / L);
+  }
+  cluster_sync_all();
+}
+
+template <int G, int M, int N, int PROBE = 0, int VQ = 0, int CL = 0>
 __global__ void __launch_bounds__(kDqThreads, 1)
     decode_dq_kernel(const pqb_cache c, const void* __restrict__ q, int q_dtype, float sm_scale_log2, EpiArgs ep,
                      WorkSplit ws, float* __restrict__ scores, int64_t scores_ld) {
@@ -394,7 +480,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   DQ_TRACE(tid == 0, 0);
 #if PQB_DQ_PRMT_TAB
-  const int tab_off = static_cast<int>(kPtTabAbs - smem_u32(smem));  // dynamic offset of the table
+  // (in a cluster launch CTA rank r's shared window starts at r << 24, scripts/micro/smem_base_cluster.cu;
+  // the PRMT-composed gather address keeps that top byte)
+  const uint32_t tab_abs = (smem_u32(smem) & 0xFF000000u) | kPtTabAbs;
+  const int tab_off = static_cast<int>(tab_abs - smem_u32(smem));  // dynamic offset of the table
   // UMMA: value tiles 1 KB aligned (the 128-byte swizzle pattern is taken from address bits 7-9)
   const int st_pad = kUmma ? static_cast<int>((1024u - (smem_u32(smem) & 1023u)) & 1023u) : 0;
   const int n_before = (tab_off - st_pad) / Cfg::kStageBytes;          // stages before the table
@@ -497,7 +586,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   }
   uint32_t u_round = 0;  // UMMA: this warpgroup's P.V rounds so far (mbarrier phases)
 #if PQB_DQ_PRMT_TAB
-  const uint32_t ptab_l = kPtTabAbs | ((lane & 15) << 3);  // this lane's bank-slot copy
+  const uint32_t ptab_l = tab_abs | ((lane & 15) << 3);  // this lane's bank-slot copy
 #else
   const uint32_t ptab_l = smem_u32(smem) + ((lane & 15) << 3);  // this lane's bank-slot copy
 #endif
@@ -555,6 +644,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           }
         }
         __syncwarp();
+      }
+      if constexpr (CL > 1) {  // the consumers' two cluster barriers (finish_cluster), before their arrive on 2
+        cluster_sync_all();
+        cluster_sync_all();
       }
       if (!first_seg) named_sync(2, kDqThreads);
       return;
@@ -1195,7 +1288,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         }
       }
     }
-    finish_segment<G>(ep, ws, unit, red, s_misc + 1, tid, kConsThreads);
+    if constexpr (CL > 1) {
+      // one segment per CTA; its merge area sits after the warps' red rows, before the table
+      finish_cluster<G, CL>(ep, unit, red, red + kNW * G * 132, tid, kConsThreads);
+    } else {
+      finish_segment<G>(ep, ws, unit, red, s_misc + 1, tid, kConsThreads);
+    }
     if constexpr (kDqWs) named_arrive(2, kDqThreads);  // producers may refill the stages
     DQ_TRACE(tid == 0 && n_seg_tr < 6, 4 + 4 * n_seg_tr);
     ++n_seg_tr;
@@ -1222,17 +1320,19 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 
 // ------------------------------------------------------------------ host side
 
-template <int G, int M, int N, int PROBE = 0, int VQ = 0>
-static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s) {
+// once per device and instance: the shared-memory opt-in (and, for the PRMT
+// build, the check that the table lands at kPtTabAbs with the stages around it)
+template <int G, int M, int N, int PROBE, int VQ, int CL>
+static int dq_prepare() {
   using Cfg = DqCfg<G, M, N, VQ>;
   static std::atomic<uint64_t> attr_done{0};
-  const int arc = once_per_device(attr_done, [] {
+  return once_per_device(attr_done, [] {
 #if PQB_DQ_PRMT_TAB
-    {  // the table must land at kPtTabAbs with the stages around it (as the kernel assumes)
+    {
       cudaFuncAttributes fa;
       int reserved = 0;
       cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, current_device());
-      if (cudaFuncGetAttributes(&fa, decode_dq_kernel<G, M, N, PROBE, VQ>) != cudaSuccess) {
+      if (cudaFuncGetAttributes(&fa, decode_dq_kernel<G, M, N, PROBE, VQ, CL>) != cudaSuccess) {
         set_error("cudaFuncGetAttributes failed");
         return PQB_ECUDA;
       }
@@ -1242,36 +1342,78 @@ static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws
       const int dyn0 = reserved + ((stat + 127) / 128) * 128;
       const int tab_off = static_cast<int>(kPtTabAbs) - dyn0;
       const int n_before = tab_off / Cfg::kStageBytes;
-      if (tab_off < 0 || n_before * Cfg::kStageBytes < kNW * G * 132 * 4 ||
+      // (cluster instances: the CTA's merge partial follows the warps' rows)
+      const int merge_bytes = kNW * G * 132 * 4 + (CL > 1 ? G * 130 * 4 : 0);
+      if (tab_off < 0 || n_before * Cfg::kStageBytes < merge_bytes ||
           tab_off + 65536 + (kNW * Cfg::kSt - n_before) * Cfg::kStageBytes > Cfg::kSmem ||
           stat + Cfg::kSmem > 232448)
         return kDqLayoutUnavailable;  // the caller falls back to the linear-layout build
     }
 #endif
-    if (cudaFuncSetAttribute(decode_dq_kernel<G, M, N, PROBE, VQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(decode_dq_kernel<G, M, N, PROBE, VQ, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              Cfg::kSmem) != cudaSuccess) {
       set_error("cudaFuncSetAttribute(smem=%d) failed", Cfg::kSmem);
       return PQB_ECUDA;
     }
     return PQB_OK;
   });
+}
+
+template <int G, int M, int N, int PROBE = 0, int VQ = 0, int CL = 0>
+static int launch_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s) {
+  using Cfg = DqCfg<G, M, N, VQ>;
+  const int arc = dq_prepare<G, M, N, PROBE, VQ, CL>();
   if (arc != PQB_OK) return arc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kDqThreads);
   cfg.dynamicSmemBytes = Cfg::kSmem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = CL > 1 ? CL : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  if (cudaLaunchKernelEx(&cfg, decode_dq_kernel<G, M, N, PROBE, VQ>, *a.cache, a.q, a.q_dtype,
+  cfg.numAttrs = CL > 1 ? 2 : 1;
+  if (cudaLaunchKernelEx(&cfg, decode_dq_kernel<G, M, N, PROBE, VQ, CL>, *a.cache, a.q, a.q_dtype,
                          a.sm_scale * kLog2e, ep, ws, a.scores, a.scores_ld) != cudaSuccess) {
     set_error("decode_dq launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     return PQB_ECUDA;
   }
   return PQB_OK;
+}
+
+// Clusters of CL CTAs of this instance that can be resident at once (0: not
+// available), cached per device.
+template <int G, int M, int N, int VQ, int CL>
+static int cluster_capacity() {
+  static std::atomic<int> cache[64];
+  std::atomic<int>& slot = cache[current_device() & 63];
+  int n = slot.load(std::memory_order_relaxed);
+  if (n != 0) return n > 0 ? n : 0;
+  using Cfg = DqCfg<G, M, N, VQ>;
+  n = -1;
+  if (dq_prepare<G, M, N, 0, VQ, CL>() == PQB_OK) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL * 64);
+    cfg.blockDim = dim3(kDqThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int c = 0;
+    if (cudaOccupancyMaxActiveClusters(&c, decode_dq_kernel<G, M, N, 0, VQ, CL>, &cfg) == cudaSuccess && c > 0) n = c;
+    else (void)cudaGetLastError();
+  }
+  slot.store(n, std::memory_order_relaxed);
+  return n > 0 ? n : 0;
 }
 
 template <int G>
@@ -1320,6 +1462,14 @@ static int dispatch_dq_mn(const DecodeArgs& a, const EpiArgs& ep, const WorkSpli
       default: handled = false; return PQB_OK;
     }
   }
+  if (ws.cluster > 1 && mn == 44) {  // aligned split, merge through distributed shared memory
+    switch (ws.cluster) {
+      case 2: return launch_dq<G, 4, 4, 0, 0, 2>(a, ep, ws, grid, s);
+      case 4: return launch_dq<G, 4, 4, 0, 0, 4>(a, ep, ws, grid, s);
+      case 8: return launch_dq<G, 4, 4, 0, 0, 8>(a, ep, ws, grid, s);
+      default: break;
+    }
+  }
   if (mn == 44 && (a.flags & PQB_DECODE_PROBE_MEM)) return launch_dq<G, 4, 4, 1>(a, ep, ws, grid, s);
   if (mn == 44 && (a.flags & PQB_DECODE_PROBE_COMPUTE)) return launch_dq<G, 4, 4, 2>(a, ep, ws, grid, s);
   switch (mn) {
@@ -1339,6 +1489,15 @@ extern "C" int pqb_debug_dq_trace(void* host, int n_ctas) {
                  cudaSuccess ? 0 : -1;
 }
 #endif
+
+int dq_cluster_capacity(int group, int mn, int value_dtype, int cl) {
+  if (mn != 44 || value_dtype != PQB_BF16) return 0;
+  if (group == 8) return cl == 2 ? cluster_capacity<8, 4, 4, 0, 2>() : cl == 4 ? cluster_capacity<8, 4, 4, 0, 4>()
+                                                                   : cl == 8 ? cluster_capacity<8, 4, 4, 0, 8>() : 0;
+  if (group == 4) return cl == 2 ? cluster_capacity<4, 4, 4, 0, 2>() : cl == 4 ? cluster_capacity<4, 4, 4, 0, 4>()
+                                                                   : cl == 8 ? cluster_capacity<4, 4, 4, 0, 8>() : 0;
+  return 0;
+}
 
 int launch_decode_dq(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s,
                      bool& handled) {

@@ -62,6 +62,16 @@ def case_decode_m3n2():
     c.decode(q, out_dtype=torch.bfloat16)
 
 
+def case_decode_cluster():
+    # 32 units of G = 8: the thread-block-cluster path (4 CTAs per unit, DSMEM merge)
+    c = _cache(4, 4, 32, 8192)
+    q = pq.normal_device((32, 8, 128), 21, dtype=torch.bfloat16)
+    a = c.decode(q)
+    b = c.decode(q, flags=pq._lib.PQB_DECODE_NO_CLUSTER)
+    torch.cuda.synchronize()
+    print("cluster vs no-cluster max abs diff", (a - b).abs().max().item())
+
+
 def case_decode_vq4():
     c = _cache(4, 4, 3, 4096, vb=4)
     q = pq.normal_device((3, 4, 128), 8, dtype=torch.bfloat16)

@@ -28,10 +28,12 @@ def _run_layer(**spec):
     from paper_2502_00527_b200 import _lib
 
     keep = spec.pop("keep")
+    flags = spec.pop("flags", 0)
     dev = torch.device("cuda", 0)
     w = bench.DecodeWorkload(dev, layers=1, page_tokens=256, seed=3, keep=keep, **spec)
+    w.base_flags = flags
     run = w.capture(w.step)
-    launches = int(_lib.load().pqb_decode_launches(w.upl, w.G, w.T, 0))
+    launches = int(_lib.load().pqb_decode_launches(w.upl, w.G, w.T, flags))
     summ = bench.parity_leg(w, keep, run)
     w.free()
     return summ, launches
@@ -61,9 +63,21 @@ def test_configs2_m3n2_128k():
     _assert_ok(summ, 12)
 
 
-def test_configs3_g8_separate_merge():
-    """configs[3] per GPU: G = 8, 32 units x 32,768 tokens, split merge in its own launch."""
+def test_configs3_g8_cluster_merge():
+    """configs[3] per GPU: G = 8, 32 units x 32,768 tokens; as benched, each unit
+    runs on a 4-CTA thread-block cluster that merges through distributed shared
+    memory (one launch)."""
     summ, launches = _run_layer(batch=32, hq=8, hkv=1, T=32768, m=4, n=4, keep=list(range(32)))
+    _assert_ok(summ, 32)
+    assert launches == 1
+
+
+def test_configs3_g8_separate_merge():
+    """configs[3] without the cluster path: balanced split, split merge in its own launch."""
+    from paper_2502_00527_b200 import _lib
+
+    summ, launches = _run_layer(batch=32, hq=8, hkv=1, T=32768, m=4, n=4, keep=list(range(32)),
+                                flags=_lib.PQB_DECODE_NO_CLUSTER)
     _assert_ok(summ, 32)
     assert launches == 2
 

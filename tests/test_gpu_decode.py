@@ -545,7 +545,10 @@ def test_decode_launch_count_policy():
     lib = pq._lib.load()
     assert lib.pqb_decode_launches(128, 4, 32768, 0) == 1  # configs[1] layer
     assert lib.pqb_decode_launches(8, 4, 4096, 0) == 2  # configs[0]: 16+ segments per unit
-    assert lib.pqb_decode_launches(32, 8, 32768, 0) == 2  # configs[3] layer
+    # configs[3] layer: the thread-block-cluster path (4 CTAs per unit, DSMEM merge) on B200, one launch;
+    # without it the split merge gets its own launch
+    assert lib.pqb_decode_launches(32, 8, 32768, 0) == 1
+    assert lib.pqb_decode_launches(32, 8, 32768, pq._lib.PQB_DECODE_NO_CLUSTER) == 2
     assert lib.pqb_decode_launches(32, 8, 4096, 0) == 1
     assert lib.pqb_decode_launches(128, 4, 32768, pq._lib.PQB_DECODE_MERGE_KERNEL) == 2
     assert lib.pqb_decode_launches(8, 4, 4096, pq._lib.PQB_DECODE_NO_COMBINE) == 1
@@ -590,6 +593,34 @@ def test_dq_split_shapes(G, values):
             for g in range(G):
                 peak_close(out[u, g], refs[u][g], OUT_RTOL_F32)
     assert pq._lib.load().pqb_decode_dq_layout() == 1  # the product table at its fixed address
+
+
+@pytest.mark.parametrize("G,U,T", [(8, 32, 8192), (4, 32, 8192), (4, 64, 8192)])
+def test_dq_cluster_merge(G, U, T):
+    """The thread-block-cluster path (units x k CTAs fill the GPU, k = 4 or 8:
+    each unit's CTAs form a cluster and LSE-merge their partials through
+    distributed shared memory): outputs within the fp32 tolerance of the oracle
+    on sampled units, one launch per call, and within fp32 round-off of the
+    non-cluster path."""
+    lib = pq._lib.load()
+    assert lib.pqb_decode_launches(U, G, T, 0) == 1
+    rng = np.random.default_rng(U + G)
+    keys = np.stack([po.synthetic_keys(T, 128, seed=2100 + u, outliers=(0, 1)) for u in range(U)])
+    vals = rng.standard_normal((U, T, 128)).astype(np.float32)
+    q = rng.standard_normal((U, G, 128)).astype(np.float32)
+    cache = pq.PolarKVCache(pq.QuantConfig(4, 4), U, 128, 0, capacity=T, page_tokens=256, value_dtype=torch.bfloat16)
+    cache.prefill(torch.from_numpy(keys).cuda(), torch.from_numpy(vals).cuda())
+    qd = torch.from_numpy(q).cuda()
+    out = cache.decode(qd).cpu().numpy()
+    alt = cache.decode(qd, flags=pq._lib.PQB_DECODE_NO_CLUSTER).cpu().numpy()
+    for u in (0, 1, U // 2, U - 1):
+        a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
+        s16 = cache.scales16[u].cpu().numpy()
+        vb = torch.from_numpy(vals[u]).to(torch.bfloat16).float().numpy().astype(np.float64)
+        for g in range(G):
+            ref = po.softmax64(po.lut_scores(q[u, g], a, r, s16, 4, 4, 1), 1.0 / math.sqrt(128)) @ vb
+            peak_close(out[u, g], ref, OUT_RTOL_F32)
+    np.testing.assert_allclose(out, alt, rtol=0, atol=1e-5 * max(1.0, float(np.abs(alt).max())))
 
 
 @pytest.mark.parametrize("G", [4, 8])
