@@ -612,6 +612,8 @@ def test_dq_cluster_merge(G, U, T):
     cache.prefill(torch.from_numpy(keys).cuda(), torch.from_numpy(vals).cuda())
     qd = torch.from_numpy(q).cuda()
     out = cache.decode(qd).cpu().numpy()
+    for _ in range(5):  # deterministic: the stage rings and the DSMEM merge leave no ordering to chance
+        assert np.array_equal(cache.decode(qd).cpu().numpy(), out)
     alt = cache.decode(qd, flags=pq._lib.PQB_DECODE_NO_CLUSTER).cpu().numpy()
     for u in (0, 1, U // 2, U - 1):
         a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
