@@ -257,6 +257,13 @@ int pqb_decode_launches(int64_t n_units, int group, int max_tokens, int flags);
  * build), 2 the linear-layout fallback (a device whose shared window is laid
  * out other than measured).  Diagnostics: tests and the bench assert 1. */
 int pqb_decode_dq_layout(void);
+/* Host-side view of the DQ kernel's cost-balanced persistent split for
+ * n_units units of max_tokens tokens on at most `ctas` CTAs: writes the CTA
+ * range starts (in 32-token tiles of the unit-major item space, n + 1 values
+ * with starts[n] = n_units * tiles) to starts (capacity >= ctas + 1) and
+ * returns n, the CTA count; 0 when the split is uniform (per_cta = ceil(items /
+ * ctas)).  No device needed (tests of the host logic). */
+int pqb_decode_split_starts(int64_t n_units, int max_tokens, int ctas, int32_t* starts);
 
 /* ------------------------------------------------------------ accessors ----
  * Tables and views the reference API exposes (all computed on the device). */

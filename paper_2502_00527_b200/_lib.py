@@ -133,6 +133,7 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     "pqb_decode_splits": (c_i32, [c_i64, c_i32]),
     "pqb_decode_launches": (c_i32, [c_i64, c_i32, c_i32, c_i32]),
     "pqb_decode_dq_layout": (c_i32, []),
+    "pqb_decode_split_starts": (c_i32, [c_i64, c_i32, c_i32, c_vp]),
     "pqb_decode_attn_peer": (
         c_i32,
         [ctypes.POINTER(PqbCache), c_i64, c_i32, c_vp, c_i32, c_f32, c_i32, ctypes.POINTER(PqbPeerOut), c_vp, c_sz,

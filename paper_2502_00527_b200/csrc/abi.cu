@@ -265,6 +265,10 @@ int pqb_decode_launches(int64_t n_units, int group, int max_tokens, int flags) {
 
 int pqb_decode_dq_layout(void) { return decode_dq_layout(); }
 
+int pqb_decode_split_starts(int64_t n_units, int max_tokens, int ctas, int32_t* starts) {
+  return starts ? decode_split_starts(n_units, max_tokens, ctas, starts) : -1;
+}
+
 int pqb_decode_splits(int64_t n_units, int max_tokens) {
   if (n_units <= 0 || max_tokens <= 0) return 1;
   return decode_splits(n_units, max_tokens);

@@ -770,8 +770,14 @@ static int dq_cluster_size(int64_t n_units, int group, int max_tokens, int flags
     return 0;
   if (c != nullptr && (c->angle_bits != 4 || c->radius_bits != 4 || c->store.value_dtype != PQB_BF16)) return 0;
   const int sms = num_sms(), tm = tiles_of(max_tokens);
+  static const int min_fill = [] {  // percent of the SMs the clusters must fill (PQB_CLUSTER_MIN_FILL, A/B)
+    const char* e = std::getenv("PQB_CLUSTER_MIN_FILL");
+    return e ? std::atoi(e) : 80;
+  }();
   for (int k : {8, 4, 2}) {
-    if (n_units * k > sms || n_units * k * 5 < static_cast<int64_t>(sms) * 4 || tm % k != 0 || tm / k < 64) continue;
+    if (n_units * k > sms || n_units * k * 100 < static_cast<int64_t>(sms) * min_fill || tm % k != 0 ||
+        tm / k < kNW)
+      continue;
     if (dq_prmt::dq_cluster_capacity(group, 44, PQB_BF16, k) < n_units) return 0;
     return k;
   }
@@ -784,6 +790,14 @@ int decode_launch_count(int64_t n_units, int group, int max_tokens, int flags) {
   if (dq_cluster_size(n_units, group, max_tokens, flags, nullptr, false, false) > 1) return 1;
   const WorkSplit ws = make_split_balanced(n_units, max_tokens, std::min(num_sms(), kMaxCtas));
   return (flags & PQB_DECODE_NO_COMBINE) || !separate_merge(flags, group, max_tokens, ws) ? 1 : 2;
+}
+
+int decode_split_starts(int64_t n_units, int max_tokens, int ctas, int32_t* starts) {
+  if (n_units <= 0 || max_tokens <= 0 || ctas <= 0 || ctas > kMaxCtas) return -1;
+  const WorkSplit w = make_split_balanced(n_units, max_tokens, ctas);
+  if (!w.balanced) return 0;
+  for (int c = 0; c <= w.n_cta; ++c) starts[c] = w.starts[c];
+  return w.n_cta;
 }
 
 static std::atomic<int> g_dq_layout{0};

@@ -60,6 +60,7 @@ int launch_radius_scales(const RadiusScalesArgs& a, cudaStream_t s);
 // decode.cu: kernels a fused DQ decode call enqueues (1, or 2 with the separate split merge)
 int decode_launch_count(int64_t n_units, int group, int max_tokens, int flags);
 int decode_dq_layout();
+int decode_split_starts(int64_t n_units, int max_tokens, int ctas, int32_t* starts);
 int launch_encode(const EncodeArgs& a, cudaStream_t s);
 // encode_fast.cu: persistent TMA-fed encoder for d = 128, m, n in {2,3,4}; false if the call does not qualify.
 bool launch_encode_fast(const EncodeArgs& a, cudaStream_t s);

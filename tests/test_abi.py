@@ -105,3 +105,28 @@ def test_store_descriptor_validation():
     rc = _lib.load().pqb_unpack_codes(ctypes.byref(st), 0, 128, 4, 4, 1, None, None, None)
     assert rc == _lib.PQB_EINVAL  # page_tokens not a multiple of 32
     assert b"page_tokens" in _lib.load().pqb_last_error()
+
+
+def test_balanced_split_host_logic():
+    """The DQ kernel's cost-balanced persistent split (decode.cu
+    make_split_balanced), host side only: CTA ranges cover the unit-major tile
+    space exactly, in order, on no more CTAs than allowed; a range that crosses
+    into a second unit is shorter than the single-unit ones (it pays a second
+    setup and merge); short launches keep the uniform split."""
+    lib = _lib.load()
+    tm = 32768 // 32
+    for units, ctas in [(128, 148), (32, 148), (64, 148), (128, 100), (5, 7)]:
+        buf = (ctypes.c_int32 * (ctas + 1))()
+        n = lib.pqb_decode_split_starts(units, 32768, ctas, buf)
+        starts = list(buf)[: n + 1]
+        assert 0 < n <= ctas
+        assert starts[0] == 0 and starts[-1] == units * tm
+        assert all(b > a for a, b in zip(starts, starts[1:]))
+        one, two = [], []
+        for a, b in zip(starts, starts[1:]):
+            (two if (b - 1) // tm != a // tm else one).append(b - a)
+        if one and two:
+            assert max(two) < max(one)
+    buf = (ctypes.c_int32 * 149)()
+    assert lib.pqb_decode_split_starts(8, 4096, 148, buf) == 0  # configs[0]: a few tiles per CTA, uniform
+    assert lib.pqb_decode_split_starts(8, 4096, 0, buf) == -1
