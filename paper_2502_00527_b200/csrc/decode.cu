@@ -682,7 +682,12 @@ size_t decode_workspace_bytes(int64_t n_units, int group, int max_tokens, int d)
 
 // Work split + epilogue arguments shared by the LUT and DQ fast kernels.
 static int fast_setup(const DecodeArgs& a, EpiArgs& ep, WorkSplit& ws, int& grid, bool balanced = false) {
-  const int ctas = a.splits > 0 ? std::min(a.splits, kMaxCtas) : std::min(num_sms(), kMaxCtas);
+  static const int ctas_env = [] {  // PQB_DQ_CTAS: persistent-grid CTA count override (A/B of grid sizes)
+    const char* e = std::getenv("PQB_DQ_CTAS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int ctas = a.splits > 0 ? std::min(a.splits, kMaxCtas)
+                                : std::min(ctas_env > 0 ? ctas_env : num_sms(), kMaxCtas);
   ws = balanced ? make_split_balanced(a.n_units, a.max_tokens, ctas) : make_split(a.n_units, a.max_tokens, ctas);
   grid = ws.balanced ? ws.n_cta : static_cast<int>((ws.items + ws.per_cta - 1) / ws.per_cta);
   ep.out = a.out;
