@@ -625,6 +625,32 @@ def test_dq_cluster_merge(G, U, T):
     np.testing.assert_allclose(out, alt, rtol=0, atol=1e-5 * max(1.0, float(np.abs(alt).max())))
 
 
+def test_dq_cluster_merge_ragged_residual():
+    """Cluster path with ragged units (some CTAs of a cluster past their unit's
+    last tile) and a residual window: within the fp32 tolerance of the oracle."""
+    U, G, res, T = 32, 8, 16, 8192
+    lens = [T if u % 3 else max(40, (u * 997) % T) for u in range(U)]
+    assert pq._lib.load().pqb_decode_launches(U, G, T, 0) == 1
+    rng = np.random.default_rng(77)
+    keys = [po.synthetic_keys(t, 128, seed=2300 + u, outliers=(0, 1)) for u, t in enumerate(lens)]
+    vals = [rng.standard_normal((t, 128)).astype(np.float32) for t in lens]
+    q = rng.standard_normal((U, G, 128)).astype(np.float32)
+    cache = pq.PolarKVCache(pq.QuantConfig(4, 4), U, 128, res, capacity=T + 1, page_tokens=256,
+                            value_dtype=torch.bfloat16)
+    for u in range(U):
+        cache.prefill(torch.from_numpy(keys[u]).cuda().unsqueeze(0), torch.from_numpy(vals[u]).cuda().unsqueeze(0),
+                      unit_start=u)
+    out = cache.decode(torch.from_numpy(q).cuda(), max_tokens=T).cpu().numpy()
+    for u in (0, 3, 6, 7, 30):
+        a, r = (t.cpu().numpy() for t in cache.code_arrays(u))
+        s16 = cache.scales16[u].cpu().numpy()
+        vb = torch.from_numpy(vals[u]).to(torch.bfloat16).float().numpy().astype(np.float64)
+        resid = keys[u][lens[u] - min(res, lens[u]):]
+        for g in range(G):
+            ref = po.softmax64(po.lut_scores(q[u, g], a, r, s16, 4, 4, 1, resid), 1.0 / math.sqrt(128)) @ vb
+            peak_close(out[u, g], ref, OUT_RTOL_F32)
+
+
 @pytest.mark.parametrize("G", [4, 8])
 def test_dq_balanced_split(G):
     """The cost-balanced persistent split (CTA ranges of >= 192 tiles, so the
