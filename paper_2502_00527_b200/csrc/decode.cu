@@ -769,7 +769,8 @@ static bool separate_merge(int flags, int group, int max_tokens, const WorkSplit
 // (resident clusters) does not qualify.
 static int dq_cluster_size(int64_t n_units, int group, int max_tokens, int flags, const pqb_cache* c,
                            bool peer, bool scores) {
-  if ((group != 4 && group != 8) || peer || scores) return 0;
+  (void)peer;  // peer mode works too: finish_cluster stores through emit(), peer_publish runs after it
+  if ((group != 4 && group != 8) || scores) return 0;
   if (flags & (PQB_DECODE_MERGE_KERNEL | PQB_DECODE_MERGE_INKERNEL | PQB_DECODE_NO_CLUSTER |
                PQB_DECODE_LUT | PQB_DECODE_DQ_LINEAR | PQB_DECODE_PROBE_MEM | PQB_DECODE_PROBE_COMPUTE))
     return 0;

@@ -27,7 +27,7 @@ def _keys(shape, layer, b, h, T):
     return po.synthetic_keys(T, 128, seed=(layer * shape.batch + b) * shape.kv_heads + h, outliers=(0, 1))
 
 
-def _worker(rank, world, port, G, result_dir):
+def _worker(rank, world, port, G, result_dir, batch=3, T=700, layers=2):
     import torch
     import torch.distributed as dist
 
@@ -38,9 +38,8 @@ def _worker(rank, world, port, G, result_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
     try:
-        shape = sh.DecodeShape(layers=2, batch=3, q_heads=2 * G, kv_heads=2)
+        shape = sh.DecodeShape(layers=layers, batch=batch, q_heads=2 * G, kv_heads=2)
         plan = sh.head_shard(shape, world, rank)
-        T = 700
         rng = np.random.default_rng(0)
         vals = rng.standard_normal((shape.layers, shape.batch, shape.kv_heads, T, 128)).astype(np.float32)
         qs = torch.from_numpy(rng.standard_normal((4, shape.layers, shape.batch, shape.q_heads, 128)).astype(np.float32))
@@ -108,13 +107,15 @@ def _worker(rank, world, port, G, result_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("G", [4, 8])
-def test_peer_gather_two_ranks_one_gpu(tmp_path, G):
+@pytest.mark.parametrize("G,shape", [(4, (3, 700, 2)), (8, (3, 700, 2)), (8, (32, 1024, 1))])
+def test_peer_gather_two_ranks_one_gpu(tmp_path, G, shape):
+    """(8, (32, 1024, 1)): each rank's layer is 32 units of G = 8, so its
+    decode runs on the thread-block-cluster path with the peer stores."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, G, str(tmp_path))) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, G, str(tmp_path), *shape)) for r in range(2)]
     for p in procs:
         p.start()
     for p in procs:
