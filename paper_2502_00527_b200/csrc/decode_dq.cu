@@ -625,21 +625,36 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           TileCursor c0, c1;
           c0.init(t_lo + w0, tpp);
           c1.init(t_lo + w1, tpp);
-          auto issue = [&](int w, uint32_t it, const TileCursor& cu) {
+          // the page base of each cursor's next tile is loaded one issue ahead (the
+          // page-table read is a dependent global load; its latency then overlaps
+          // the wait for the stage instead of following it)
+          auto page_of = [&](const TileCursor& cu) {
+            return page_base_c(c.store, unit, PROBE == 2 ? 0 : (cu.tile < t_hi ? cu.pg : 0));
+          };
+          auto issue = [&](int w, uint32_t it, const TileCursor& cu, const uint8_t* pb) {
             const uint32_t s = it % kSt;
             // the ring starts empty: the first kSt fills need no release
             if (it >= kSt) mbar_wait(&s_empty[w][s], ((it / kSt) & 1) ^ 1);
             fence_proxy_async_smem();
-            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(w * kSt + s), c.store,
-                                    page_base_c(c.store, unit, PROBE == 2 ? 0 : cu.pg), PROBE == 2 ? 0 : cu.tin,
-                                    &s_bar[w][s]);
+            issue_tile_dq<M, N, VQ, kScores>(stage_ptr(w * kSt + s), c.store, pb, PROBE == 2 ? 0 : cu.tin,
+                                             &s_bar[w][s]);
           };
+          const uint8_t* pb0 = page_of(c0);
+          const uint8_t* pb1 = page_of(c1);
           while (c0.tile < t_hi) {  // c1 runs 4 tiles behind c0's stream position, never past it
-            issue(w0, it0++, c0);
-            c0.next(dpg, dtin, tpp);
+            TileCursor n0 = c0;
+            n0.next(dpg, dtin, tpp);
+            const uint8_t* nb0 = page_of(n0);
+            issue(w0, it0++, c0, pb0);
+            c0 = n0;
+            pb0 = nb0;
             if (c1.tile < t_hi) {
-              issue(w1, it1++, c1);
-              c1.next(dpg, dtin, tpp);
+              TileCursor n1 = c1;
+              n1.next(dpg, dtin, tpp);
+              const uint8_t* nb1 = page_of(n1);
+              issue(w1, it1++, c1, pb1);
+              c1 = n1;
+              pb1 = nb1;
             }
           }
         }
