@@ -251,6 +251,10 @@ PQB_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                : "memory");
 }
 
+#ifndef PQB_MBAR_SLEEP_NS
+#define PQB_MBAR_SLEEP_NS 20000
+#endif
+
 PQB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
   uint32_t ok;
   asm volatile(
@@ -265,6 +269,26 @@ PQB_DEV bool mbar_try_wait(uint64_t* bar, uint32_t phase) {
 
 PQB_DEV void mbar_wait(uint64_t* bar, uint32_t phase) {
   while (!mbar_try_wait(bar, phase)) {
+  }
+}
+
+// try_wait with a suspend-time hint: the thread sleeps in the barrier unit
+// until the phase completes (or the hint, in ns, expires) instead of spinning
+// through try_wait / branch / yield -- a spinning producer lane otherwise
+// takes issue slots (and power) from the compute warps of its sub-partition.
+PQB_DEV bool mbar_try_wait_sleep(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase), "r"(PQB_MBAR_SLEEP_NS)
+      : "memory");
+  return ok != 0;
+}
+PQB_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  while (!mbar_try_wait_sleep(bar, phase)) {
   }
 }
 

@@ -68,6 +68,14 @@ namespace PQB_DQ_NS {
 // the TMA issue code off the compute warps; registers are rebalanced with
 // setmaxnreg (compute warps 232, producers 40: 2 x 128 x 232 + 128 x 40 <= 64K).
 // PQB_DQ_WS=0 builds the previous layout (lane 0 of each compute warp issues).
+// mbarrier waits with a suspend-time hint (common.cuh mbar_wait_sleep) for the
+// producers' empty-slot waits and the compute warps' full-slot waits
+#ifndef PQB_DQ_SLEEP_PROD
+#define PQB_DQ_SLEEP_PROD 1
+#endif
+#ifndef PQB_DQ_SLEEP_CONS
+#define PQB_DQ_SLEEP_CONS 1
+#endif
 #ifndef PQB_DQ_WS
 #define PQB_DQ_WS 1
 #endif
@@ -634,7 +642,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           auto issue = [&](int w, uint32_t it, const TileCursor& cu, const uint8_t* pb) {
             const uint32_t s = it % kSt;
             // the ring starts empty: the first kSt fills need no release
-            if (it >= kSt) mbar_wait(&s_empty[w][s], ((it / kSt) & 1) ^ 1);
+            if (it >= kSt) {
+              if constexpr (PQB_DQ_SLEEP_PROD) mbar_wait_sleep(&s_empty[w][s], ((it / kSt) & 1) ^ 1);
+              else mbar_wait(&s_empty[w][s], ((it / kSt) & 1) ^ 1);
+            }
             fence_proxy_async_smem();
             issue_tile_dq<M, N, VQ, kScores>(stage_ptr(w * kSt + s), c.store, pb, PROBE == 2 ? 0 : cu.tin,
                                              &s_bar[w][s]);
@@ -880,7 +891,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
         float x[4][2];
         if (has) {
           s = k_iter % kSt;
-          mbar_wait(bar + s, (k_iter / kSt) & 1);
+          if constexpr (PQB_DQ_SLEEP_CONS) mbar_wait_sleep(bar + s, (k_iter / kSt) & 1);
+      else mbar_wait(bar + s, (k_iter / kSt) & 1);
           st = stage_ptr(warp * kSt + s);
           tile_scores(st, tok0, x);
         }
@@ -1017,7 +1029,8 @@ __global__ void __launch_bounds__(kDqThreads, 1)
     for (int tile = first; tile < t_hi; tile += kNW, ++k_iter) {
       const uint32_t s = k_iter % kSt;
       const int nt = tile + kSt * kNW;  // the tile this stage is refilled with
-      mbar_wait(bar + s, (k_iter / kSt) & 1);
+      if constexpr (PQB_DQ_SLEEP_CONS) mbar_wait_sleep(bar + s, (k_iter / kSt) & 1);
+      else mbar_wait(bar + s, (k_iter / kSt) & 1);
       const uint8_t* st = stage_ptr(warp * kSt + s);
       const int tok0 = tile * kTile;
       if constexpr (PROBE == 1) {
