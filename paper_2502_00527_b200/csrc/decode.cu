@@ -781,8 +781,11 @@ static int dq_cluster_size(int64_t n_units, int group, int max_tokens, int flags
     return e ? std::atoi(e) : 80;
   }();
   for (int k : {8, 4, 2}) {
-    if (n_units * k > sms || n_units * k * 100 < static_cast<int64_t>(sms) * min_fill || tm % k != 0 ||
-        tm / k < kNW)
+    // short launches (<= 32 tiles per CTA: latency-bound, e.g. configs[0]) take the
+    // cluster path from 40 % of the SMs: one launch instead of decode + merge
+    // (configs[0] 14.4-15.6 -> 12.7 us per single-layer graph, scripts/small_cluster_probe.py)
+    const int fill = tm / k <= 32 ? std::min(min_fill, 40) : min_fill;
+    if (n_units * k > sms || n_units * k * 100 < static_cast<int64_t>(sms) * fill || tm % k != 0 || tm / k < kNW)
       continue;
     if (dq_prmt::dq_cluster_capacity(group, 44, PQB_BF16, k) < n_units) return 0;
     return k;

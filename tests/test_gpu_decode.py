@@ -544,7 +544,9 @@ def test_decode_launch_count_policy():
     NO_COMBINE; a merge-kernel shape still decodes to the LUT path's outputs."""
     lib = pq._lib.load()
     assert lib.pqb_decode_launches(128, 4, 32768, 0) == 1  # configs[1] layer
-    assert lib.pqb_decode_launches(8, 4, 4096, 0) == 2  # configs[0]: 16+ segments per unit
+    # configs[0]: a short launch, on 8-CTA clusters (one launch); without them 16+ segments per unit
+    assert lib.pqb_decode_launches(8, 4, 4096, 0) == 1
+    assert lib.pqb_decode_launches(8, 4, 4096, pq._lib.PQB_DECODE_NO_CLUSTER) == 2
     # configs[3] layer: the thread-block-cluster path (4 CTAs per unit, DSMEM merge) on B200, one launch;
     # without it the split merge gets its own launch
     assert lib.pqb_decode_launches(32, 8, 32768, 0) == 1
