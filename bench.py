@@ -367,7 +367,10 @@ class DecodeWorkload:
 
         if self.peers is not None:
             return 2 * self.L
-        return self.L * int(_lib.load().pqb_decode_launches(self.upl, self.G, self.T, self.base_flags))
+        vdt = {"bf16": _lib.PQB_BF16, "f32": _lib.PQB_F32, "vq2": _lib.PQB_VQ2, "vq4": _lib.PQB_VQ4,
+               "vq8": _lib.PQB_VQ8}[self.values]
+        return self.L * int(_lib.load().pqb_decode_launches_ex(self.upl, self.G, self.T, self.base_flags, self.m,
+                                                               self.n, vdt))
 
     def bytes_per_launch(self) -> int:
         return self.upl * unit_bytes(self.T, self.G, 128, self.m, self.n, self.values)

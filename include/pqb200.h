@@ -252,6 +252,11 @@ int pqb_decode_splits(int64_t n_units, int max_tokens);
 /* Kernels one fused DQ decode call (group 4 or 8, out != NULL, no peers) enqueues
  * for this shape and flags: 1, or 2 when the split merge runs as its own launch. */
 int pqb_decode_launches(int64_t n_units, int group, int max_tokens, int flags);
+/* The same for a store of angle_bits / radius_bits codes and value_dtype
+ * values (pqb_store.value_dtype): the thread-block-cluster path (one launch)
+ * needs m = n = 4 with bf16 values; pqb_decode_launches assumes that store. */
+int pqb_decode_launches_ex(int64_t n_units, int group, int max_tokens, int flags, int angle_bits, int radius_bits,
+                           int value_dtype);
 /* Shared-memory layout the last fused DQ launch in this process used: 0 none
  * yet, 1 the product table at its fixed shared-window address (the fast
  * build), 2 the linear-layout fallback (a device whose shared window is laid

@@ -132,6 +132,7 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
     ),
     "pqb_decode_splits": (c_i32, [c_i64, c_i32]),
     "pqb_decode_launches": (c_i32, [c_i64, c_i32, c_i32, c_i32]),
+    "pqb_decode_launches_ex": (c_i32, [c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32]),
     "pqb_decode_dq_layout": (c_i32, []),
     "pqb_decode_split_starts": (c_i32, [c_i64, c_i32, c_i32, c_vp]),
     "pqb_decode_attn_peer": (

@@ -263,6 +263,12 @@ int pqb_decode_launches(int64_t n_units, int group, int max_tokens, int flags) {
   return decode_launch_count(n_units, group, max_tokens, flags);
 }
 
+int pqb_decode_launches_ex(int64_t n_units, int group, int max_tokens, int flags, int angle_bits, int radius_bits,
+                           int value_dtype) {
+  if (n_units <= 0 || max_tokens <= 0) return 1;
+  return decode_launch_count(n_units, group, max_tokens, flags, angle_bits, radius_bits, value_dtype);
+}
+
 int pqb_decode_dq_layout(void) { return decode_dq_layout(); }
 
 int pqb_decode_split_starts(int64_t n_units, int max_tokens, int ctas, int32_t* starts) {

@@ -793,10 +793,14 @@ static int dq_cluster_size(int64_t n_units, int group, int max_tokens, int flags
   return 0;
 }
 
-int decode_launch_count(int64_t n_units, int group, int max_tokens, int flags) {
+int decode_launch_count(int64_t n_units, int group, int max_tokens, int flags, int angle_bits, int radius_bits,
+                       int value_dtype) {
   if (group != 4 && group != 8) return 1;
-  // (the cluster path needs m = n = 4 with bf16 values; the count assumes that store)
-  if (dq_cluster_size(n_units, group, max_tokens, flags, nullptr, false, false) > 1) return 1;
+  pqb_cache probe = {};  // only the fields dq_cluster_size reads
+  probe.angle_bits = angle_bits;
+  probe.radius_bits = radius_bits;
+  probe.store.value_dtype = value_dtype;
+  if (dq_cluster_size(n_units, group, max_tokens, flags, &probe, false, false) > 1) return 1;
   const WorkSplit ws = make_split_balanced(n_units, max_tokens, std::min(num_sms(), kMaxCtas));
   return (flags & PQB_DECODE_NO_COMBINE) || !separate_merge(flags, group, max_tokens, ws) ? 1 : 2;
 }

@@ -58,7 +58,8 @@ struct DecodeArgs {
 
 int launch_radius_scales(const RadiusScalesArgs& a, cudaStream_t s);
 // decode.cu: kernels a fused DQ decode call enqueues (1, or 2 with the separate split merge)
-int decode_launch_count(int64_t n_units, int group, int max_tokens, int flags);
+int decode_launch_count(int64_t n_units, int group, int max_tokens, int flags, int angle_bits = 4, int radius_bits = 4,
+                       int value_dtype = PQB_BF16);
 int decode_dq_layout();
 int decode_split_starts(int64_t n_units, int max_tokens, int ctas, int32_t* starts);
 int launch_encode(const EncodeArgs& a, cudaStream_t s);

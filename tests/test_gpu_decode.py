@@ -547,6 +547,11 @@ def test_decode_launch_count_policy():
     # configs[0]: a short launch, on 8-CTA clusters (one launch); without them 16+ segments per unit
     assert lib.pqb_decode_launches(8, 4, 4096, 0) == 1
     assert lib.pqb_decode_launches(8, 4, 4096, pq._lib.PQB_DECODE_NO_CLUSTER) == 2
+    # the cluster path needs m = n = 4 with bf16 values; other stores keep the merge launch
+    bf16, vq4 = pq._lib.PQB_BF16, pq._lib.PQB_VQ4
+    assert lib.pqb_decode_launches_ex(32, 8, 32768, 0, 4, 4, bf16) == 1
+    assert lib.pqb_decode_launches_ex(32, 8, 32768, 0, 3, 2, bf16) == 2
+    assert lib.pqb_decode_launches_ex(32, 8, 32768, 0, 4, 4, vq4) == 2
     # configs[3] layer: the thread-block-cluster path (4 CTAs per unit, DSMEM merge) on B200, one launch;
     # without it the split merge gets its own launch
     assert lib.pqb_decode_launches(32, 8, 32768, 0) == 1
