@@ -334,8 +334,11 @@ class DecodeWorkload:
         if plan is not None and gather == "p2p":  # fused into the decode epilogue (peer stores + flags)
             from paper_2502_00527_b200.sharding import PeerGather
 
-            self.peers = PeerGather(plan, dev, group)
-        elif plan is not None:
+            try:
+                self.peers = PeerGather(plan, dev, group)
+            except RuntimeError as exc:  # no P2P between the ranks' GPUs: the NCCL all-gather instead
+                print(f"[bench] {exc}; using the NCCL gather", file=sys.stderr, flush=True)
+        if plan is not None and self.peers is None:
             self.gathered = torch.empty((layers, batch, hq, 128), dtype=torch.bfloat16, device=dev)
         self.stream = torch.cuda.Stream(device=dev)
         # the prefill ran on the current stream; every decode runs on self.stream
@@ -489,6 +492,8 @@ class DecodeWorkload:
 
     def free(self):
         del self.cache, self.q, self.out, self.views, self.kept
+        if self.peers is not None:
+            self.peers.close()  # collective: every rank frees its workloads in the same order
         self.peers = None
         self.torch.cuda.empty_cache()
 
@@ -758,6 +763,8 @@ def run_extras(dev, a, rank: int, world: int, dist) -> dict:
             r["bytes_per_step_per_gpu"] = w.L * w.bytes_per_launch()
             if keep:
                 r["parity"] = parity_leg(w, keep, run, dist)
+            r["gather"] = ("fused into the decode epilogue (peer stores, CUDA IPC)" if w.peers is not None
+                           else "NCCL all-gather (no P2P access between the ranks' GPUs)")
             w.free()
             del w
             torch.cuda.empty_cache()

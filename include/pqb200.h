@@ -247,6 +247,21 @@ int pqb_decode_attn_peer(const pqb_cache* cache, int64_t n_units, int group, con
  * flags[k] >= *expect for every k != rank (acquire loads, system scope).  After
  * it the layer's gathered buffer is complete. */
 int pqb_peer_wait(const uint32_t* flags, int n_peers, int rank, uint32_t* expect, pqb_stream_t stream);
+/* Peer-visible buffers for pqb_peer_out (one process per GPU).  The owner
+ * allocates with pqb_ipc_alloc on `device` (cudaMalloc, zero-filled, so the
+ * handle names the allocation's base) and sends the PQB_IPC_HANDLE_BYTES
+ * handle to the other ranks; each of them maps it with pqb_ipc_open into ITS
+ * OWN device's address space (peer access enabled on first use), so the
+ * decode kernel running on that device can store into it over NVLink.
+ * pqb_ipc_close unmaps an opened buffer; pqb_ipc_free releases an owned one
+ * (after every importer has closed it).  pqb_peer_access reports whether
+ * `device` can reach `peer_device` (1) or not (0). */
+#define PQB_IPC_HANDLE_BYTES 64
+int pqb_ipc_alloc(int device, size_t bytes, void** ptr, void* handle);
+int pqb_ipc_open(int device, const void* handle, void** ptr);
+int pqb_ipc_close(int device, void* ptr);
+int pqb_ipc_free(int device, void* ptr);
+int pqb_peer_access(int device, int peer_device, int* can_access);
 
 int pqb_decode_splits(int64_t n_units, int max_tokens);
 /* Kernels one fused DQ decode call (group 4 or 8, out != NULL, no peers) enqueues

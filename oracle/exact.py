@@ -14,7 +14,14 @@ _lib = None
 
 
 def build() -> Path:
-    subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
+    """make under an exclusive file lock (ranks of a multi-process bench may
+    all ask for the checker at once; the Makefile also renames atomically)."""
+    import fcntl
+
+    (HERE / "build").mkdir(exist_ok=True)
+    with open(HERE / "build" / ".lock", "w") as fh:
+        fcntl.flock(fh, fcntl.LOCK_EX)
+        subprocess.run(["make", "-s", "-C", str(HERE)], check=True)
     return LIB
 
 

@@ -70,6 +70,7 @@ class PqbCache(ctypes.Structure):
 
 
 PQB_MAX_PEERS = 8
+PQB_IPC_HANDLE_BYTES = 64
 
 
 class PqbPeerOut(ctypes.Structure):
@@ -141,6 +142,11 @@ SIGNATURES: dict[str, tuple[object, list[object]]] = {
          c_vp],
     ),
     "pqb_peer_wait": (c_i32, [c_vp, c_i32, c_i32, c_vp, c_vp]),
+    "pqb_ipc_alloc": (c_i32, [c_i32, c_sz, ctypes.POINTER(c_vp), c_vp]),
+    "pqb_ipc_open": (c_i32, [c_i32, c_vp, ctypes.POINTER(c_vp)]),
+    "pqb_ipc_close": (c_i32, [c_i32, c_vp]),
+    "pqb_ipc_free": (c_i32, [c_i32, c_vp]),
+    "pqb_peer_access": (c_i32, [c_i32, c_i32, ctypes.POINTER(c_i32)]),
     "pqb_angle_table": (c_i32, [c_i32, c_vp, c_vp, c_vp]),
     "pqb_query_lut": (c_i32, [c_vp, c_i32, c_i64, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "pqb_radius_table": (c_i32, [c_vp, c_i64, c_i32, c_i32, c_vp, c_vp]),

@@ -2,6 +2,7 @@
 // kernel launchers, and status / thread-local error reporting (include/pqb200.h).
 #include <cstdarg>
 #include <cstdio>
+#include <cstring>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -256,6 +257,75 @@ int pqb_peer_wait(const uint32_t* flags, int n_peers, int rank, uint32_t* expect
             "bad peer wait arguments");
   launch_peer_wait(flags, n_peers, rank, expect, reinterpret_cast<cudaStream_t>(stream));
   return cuda_status("pqb_peer_wait");
+}
+
+// ---- peer-visible buffers (pqb_peer_out over CUDA IPC)
+static int rt_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return PQB_OK;
+  (void)cudaGetLastError();
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  return PQB_ECUDA;
+}
+
+static int select_device(int device) {
+  int n = 0;
+  PQB_CHECK(cudaGetDeviceCount(&n) == cudaSuccess && device >= 0 && device < n, PQB_EINVAL,
+            "device %d out of range (%d visible)", device, n);
+  return rt_status(cudaSetDevice(device), "cudaSetDevice");
+}
+
+int pqb_ipc_alloc(int device, size_t bytes, void** ptr, void* handle) {
+  PQB_CHECK(ptr && handle && bytes > 0, PQB_EINVAL, "pqb_ipc_alloc: null output or zero size");
+  *ptr = nullptr;
+  int rc = select_device(device);
+  if (rc != PQB_OK) return rc;
+  void* p = nullptr;
+  if ((rc = rt_status(cudaMalloc(&p, bytes), "cudaMalloc")) != PQB_OK) return rc;
+  cudaIpcMemHandle_t h;
+  rc = rt_status(cudaMemset(p, 0, bytes), "cudaMemset");
+  if (rc == PQB_OK) rc = rt_status(cudaIpcGetMemHandle(&h, p), "cudaIpcGetMemHandle");
+  if (rc != PQB_OK) {
+    cudaFree(p);
+    return rc;
+  }
+  static_assert(sizeof(h) == PQB_IPC_HANDLE_BYTES, "IPC handle size");
+  memcpy(handle, &h, sizeof(h));
+  *ptr = p;
+  return PQB_OK;
+}
+
+int pqb_ipc_open(int device, const void* handle, void** ptr) {
+  PQB_CHECK(ptr && handle, PQB_EINVAL, "pqb_ipc_open: null handle or output");
+  *ptr = nullptr;
+  const int rc = select_device(device);
+  if (rc != PQB_OK) return rc;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  return rt_status(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+int pqb_ipc_close(int device, void* ptr) {
+  PQB_CHECK(ptr, PQB_EINVAL, "pqb_ipc_close: null pointer");
+  const int rc = select_device(device);
+  return rc != PQB_OK ? rc : rt_status(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
+}
+
+int pqb_ipc_free(int device, void* ptr) {
+  PQB_CHECK(ptr, PQB_EINVAL, "pqb_ipc_free: null pointer");
+  const int rc = select_device(device);
+  return rc != PQB_OK ? rc : rt_status(cudaFree(ptr), "cudaFree");
+}
+
+int pqb_peer_access(int device, int peer_device, int* can_access) {
+  PQB_CHECK(can_access, PQB_EINVAL, "pqb_peer_access: null output");
+  int n = 0;
+  PQB_CHECK(cudaGetDeviceCount(&n) == cudaSuccess && device >= 0 && device < n && peer_device >= 0 &&
+                peer_device < n, PQB_EINVAL, "devices %d, %d out of range (%d visible)", device, peer_device, n);
+  if (device == peer_device) {
+    *can_access = 1;
+    return PQB_OK;
+  }
+  return rt_status(cudaDeviceCanAccessPeer(can_access, device, peer_device), "cudaDeviceCanAccessPeer");
 }
 
 int pqb_decode_launches(int64_t n_units, int group, int max_tokens, int flags) {

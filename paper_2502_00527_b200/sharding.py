@@ -142,13 +142,38 @@ def plan_for(shape: DecodeShape, world: int, rank: int, head: bool) -> ShardPlan
     return head_shard(shape, world, rank) if head else batch_shard(shape, world, rank)
 
 
+class _DeviceArray:
+    """__cuda_array_interface__ view of raw device memory (torch.as_tensor wraps it)."""
+
+    def __init__(self, ptr: int, shape: tuple, typestr: str) -> None:
+        self.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (ptr, False),
+                                         "strides": None, "version": 3}
+
+
+def peer_gather_supported(device, world_devices) -> bool:
+    """True when ``device`` can store into every device in ``world_devices``
+    (the fused gather's peer stores; NVLink/NVSwitch boxes: all pairs)."""
+    from . import _lib
+    import ctypes
+
+    dev = torch.device(device).index or 0
+    for other in world_devices:
+        can = _lib.c_i32(0)
+        _lib.call("pqb_peer_access", dev, int(other), ctypes.byref(can))
+        if not can.value:
+            return False
+    return True
+
+
 class PeerGather:
     """Gathered per-layer outputs [2, L, B, Hq, d] shared by the ranks of one node.
 
     Every rank allocates its own buffer and a flag array [L, world] (uint32,
-    zero), then all ranks exchange CUDA IPC handles (torch's CUDA tensor
-    reduction, sent through ``dist.all_gather_object``) and open each other's
-    buffers, so the decode epilogue can store into all of them directly.
+    zero) with ``pqb_ipc_alloc`` (plain cudaMalloc, so the IPC handle names
+    the allocation), the ranks exchange the handles (``dist.all_gather_object``)
+    and each maps the others' buffers into ITS OWN device's address space with
+    ``pqb_ipc_open`` (peer access enabled on first use), so the decode
+    epilogue running on that device can store into all of them over NVLink.
 
     Steps alternate between two buffers (``parity``).  Step k's decode writes
     buffer k % 2 of every peer once the writing rank has seen step k - 1
@@ -157,33 +182,90 @@ class PeerGather:
     k - 2's outputs (buffer k % 2).  Contract: a rank consumes step k's
     outputs (``out[k % 2]``) on its decode stream before it enqueues step
     k + 2's decode.  With one buffer a fast rank's step k + 1 stores could
-    overwrite rows a slow rank had not yet read."""
+    overwrite rows a slow rank had not yet read.  ``close()`` (collective)
+    unmaps the peers' buffers and frees this rank's."""
 
     def __init__(self, plan: ShardPlan, device, group=None, dtype=torch.bfloat16) -> None:
+        import ctypes
+
         import torch.distributed as dist
-        from torch.multiprocessing.reductions import reduce_tensor
+
+        from . import _lib
 
         S = plan.shape
         if plan.world > 8:
             raise ValueError("peer gather supports up to 8 ranks")
-        self.plan, self.dtype = plan, dtype
-        self.out = torch.zeros((2, S.layers, S.batch, S.q_heads, S.head_dim), dtype=dtype, device=device)
-        self.flags = torch.zeros((S.layers, plan.world), dtype=torch.int32, device=device)  # counts, peers add
-        self.expect = torch.zeros(S.layers, dtype=torch.int32, device=device)  # this rank's per-layer count
+        if dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError(f"peer gather outputs are bf16 or fp32, got {dtype}")
+        self.plan, self.dtype, self.group = plan, dtype, group
+        self.device = torch.device(device)
+        self.dev = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        out_shape = (2, S.layers, S.batch, S.q_heads, S.head_dim)
+        esz = 2 if dtype == torch.bfloat16 else 4
+        self._out_bytes = 2 * S.layers * S.batch * S.q_heads * S.head_dim * esz
+        self._layer_bytes = S.batch * S.q_heads * S.head_dim * esz
+        self._flag_bytes = S.layers * plan.world * 4
+        torch.cuda.synchronize(self.device)
+        # every rank must reach every other rank's device (collective verdict, so
+        # all ranks raise together and a caller can fall back to the NCCL gather)
+        devs = [None] * plan.world
+        dist.all_gather_object(devs, self.dev, group=group)
+        ok = [None] * plan.world
+        dist.all_gather_object(ok, peer_gather_supported(self.device, set(devs)), group=group)
+        if not all(ok):
+            raise RuntimeError(f"peer gather: no P2P access between the ranks' devices {devs}")
+        self._own = []  # (ptr) allocated here, freed by close()
+        self._opened = []  # peer mappings, unmapped by close()
+        mine = []
+        for nbytes in (self._out_bytes, self._flag_bytes):
+            p, h = ctypes.c_void_p(), ctypes.create_string_buffer(_lib.PQB_IPC_HANDLE_BYTES)
+            _lib.call("pqb_ipc_alloc", self.dev, nbytes, ctypes.byref(p), h)
+            self._own.append(p.value)
+            mine.append(h.raw)
+        raw_out = torch.as_tensor(_DeviceArray(self._own[0], (self._out_bytes // esz,), "<i2" if esz == 2 else "<f4"),
+                                  device=self.device)
+        self.out = (raw_out.view(torch.bfloat16) if esz == 2 else raw_out).view(out_shape)
+        self.flags = torch.as_tensor(_DeviceArray(self._own[1], (S.layers, plan.world), "<i4"),
+                                     device=self.device)  # counts, peers add
+        self.expect = torch.zeros(S.layers, dtype=torch.int32, device=self.device)  # this rank's per-layer count
         self.parity = 0
-        torch.cuda.synchronize(device)
-        mine = (reduce_tensor(self.out), reduce_tensor(self.flags))
         handles = [None] * plan.world
         dist.all_gather_object(handles, mine, group=group)
-        self.peer_out, self.peer_flags = [], []
+        self.peer_out, self.peer_flags = [], []  # raw base pointers on this device
         for r, (ho, hf) in enumerate(handles):
             if r == plan.rank:
-                self.peer_out.append(self.out)
-                self.peer_flags.append(self.flags)
-            else:
-                self.peer_out.append(ho[0](*ho[1]))
-                self.peer_flags.append(hf[0](*hf[1]))
+                self.peer_out.append(self._own[0])
+                self.peer_flags.append(self._own[1])
+                continue
+            ptrs = []
+            for h in (ho, hf):
+                p = ctypes.c_void_p()
+                _lib.call("pqb_ipc_open", self.dev, ctypes.create_string_buffer(h, len(h)), ctypes.byref(p))
+                self._opened.append(p.value)
+                ptrs.append(p.value)
+            self.peer_out.append(ptrs[0])
+            self.peer_flags.append(ptrs[1])
         self._desc = [[self._descriptor(p, layer) for layer in range(S.layers)] for p in range(2)]
+
+    def close(self) -> None:
+        """Collective: unmap the peers' buffers, then free this rank's own
+        (every rank must have unmapped it first)."""
+        import torch.distributed as dist
+
+        from . import _lib
+
+        if not self._own:
+            return
+        torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.group)
+        for p in self._opened:
+            _lib.call("pqb_ipc_close", self.dev, p)
+        self._opened = []
+        dist.barrier(group=self.group)
+        self.out = self.flags = None
+        for p in self._own:
+            _lib.call("pqb_ipc_free", self.dev, p)
+        self._own = []
 
     def next_step(self) -> int:
         """Start a step: flip to the other buffer; returns its parity."""
@@ -203,8 +285,8 @@ class PeerGather:
         p, S = self.plan, self.plan.shape
         d = _lib.PqbPeerOut()
         for k in range(p.world):
-            d.out[k] = self.peer_out[k][parity, layer].data_ptr()
-            d.flags[k] = self.peer_flags[k][layer].data_ptr()
+            d.out[k] = self.peer_out[k] + (parity * S.layers + layer) * self._layer_bytes
+            d.flags[k] = self.peer_flags[k] + layer * p.world * 4
         d.n_peers, d.rank = p.world, p.rank
         d.batch0, d.head0, d.kv_local, d.q_heads = p.b0, p.h0, p.kv_heads, S.q_heads
         d.out_dtype = dtype_code(self.out)

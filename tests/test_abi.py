@@ -81,6 +81,11 @@ def test_peer_descriptor_validation():
         lambda L: L.pqb_peer_wait(None, 2, 0, None, None),  # null flags
         lambda L: L.pqb_decode_attn_peer(None, 1, 4, None, 1, 1.0, 16, None, None, 0, None),  # null peer
         lambda L: L.pqb_store_values_ex(None, 1, 1, 1, 7, 0, 0, None, None, 0, None, None),  # odd d
+        lambda L: L.pqb_ipc_alloc(0, 0, None, None),  # null outputs, zero size
+        lambda L: L.pqb_ipc_open(0, None, None),  # null handle
+        lambda L: L.pqb_ipc_close(0, None),
+        lambda L: L.pqb_ipc_free(0, None),
+        lambda L: L.pqb_peer_access(0, 0, None),  # null output
     ],
 )
 def test_validation_maps_to_value_error(call):
