@@ -516,7 +516,9 @@ def parity_leg(w: DecodeWorkload, units, run, dist=None) -> dict:
     with w.torch.cuda.stream(w.stream):
         run()
     w.torch.cuda.synchronize(w.dev)
-    results = parity.check_many(w.parity_jobs(units))
+    # the host's cores shared by the ranks on this node
+    threads = max(1, len(os.sched_getaffinity(0)) // max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1"))))
+    results = parity.check_many(w.parity_jobs(units), threads=threads)
     summ = parity.summarize(results)
     summ["seconds"] = time.perf_counter() - t0
     if dist:
@@ -556,7 +558,9 @@ def run_ours(a, rank: int, world: int, dist) -> dict | None:
         shape = sharding.DecodeShape(a.layers, a.batch, a.hq, a.hkv)
         plan = sharding.head_shard(shape, world, rank)
     upl = plan.units_per_layer if plan is not None else a.batch * a.hkv
-    keep = [] if a.no_parity or a.profile else sample_units(upl, a.layers, a.parity_sample, 77 + rank)
+    # every unit of layer 0 on rank 0; the other ranks a random sample
+    keep = ([] if a.no_parity or a.profile
+            else sample_units(upl, a.layers, a.parity_sample, 77 + rank, all_layer0=rank == 0))
     w = DecodeWorkload(dev, layers=a.layers, batch=batch, hq=a.hq, hkv=a.hkv, T=a.ctx, m=a.m, n=a.n,
                        page_tokens=a.page_tokens, seed=rank, plan=plan, gather=a.gather, values=a.values,
                        keep=keep, group=None)
