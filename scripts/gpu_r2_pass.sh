@@ -9,7 +9,3 @@ timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpur
 if [ "${MULTI:-1}" = "1" ]; then
 timeout 900 python bench.py --gpus 2 --no-cpu > gpurun_out/bench_g2.json 2> gpurun_out/bench_g2.err; echo "g2 rc=$?"; tail -3 gpurun_out/bench_g2.err
 fi
-for tool in memcheck synccheck; do
-  timeout 600 compute-sanitizer --print-limit 10 --error-exitcode 9 --tool $tool python scripts/sanitize.py decode_cluster > gpurun_out/${tool}_decode_cluster.log 2>&1
-  echo "$tool decode_cluster rc=$? $(grep -E 'ERROR SUMMARY' gpurun_out/${tool}_decode_cluster.log | tail -1)"
-done
