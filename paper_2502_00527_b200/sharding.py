@@ -336,6 +336,12 @@ class HeadShardedDecoder:
         if self.peers is not None:
             self.peers.next_step()
 
+    def close(self) -> None:
+        """Collective (p2p): release the shared gather buffers (PeerGather.close)."""
+        if self.peers is not None:
+            self.peers.close()
+            self.peers = None
+
     def step(self, q: torch.Tensor) -> torch.Tensor:
         """All layers for q [L, B, Hq, d]; returns a fresh [L, B, Hq, d]
         (copied on the decode stream, as the double-buffer contract needs)."""

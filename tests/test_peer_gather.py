@@ -102,6 +102,9 @@ def _worker(rank, world, port, G, result_dir, batch=3, T=700, layers=2):
         ref = ref_of(q)
         errs = [err(g, ref) for g in got] + [err(e, ref_of(qs[i])) for i, e in enumerate(eager)]
         np.save(os.path.join(result_dir, f"rank{rank}.npy"), np.array(errs))
+        del graph
+        dec.close()  # collective: peers unmapped, own buffers freed
+        assert dec.peers is None
         dist.barrier()
     finally:
         dist.destroy_process_group()
