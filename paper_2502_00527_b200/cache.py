@@ -534,6 +534,17 @@ class UnitView:
     def max_tokens(self) -> int:
         return int(self.cache.host_seq[self.u0 : self.u1].max())
 
+    def _t_max(self, max_tokens: int | None) -> int:
+        """Tile bound of a launch: the view's longest unit, or a caller bound
+        (e.g. a graph captured at capacity) that must not be below it -- the
+        kernels cut each unit's tiles at this bound and size score rows by it."""
+        actual = self.max_tokens
+        if max_tokens is None:
+            return actual
+        if int(max_tokens) < actual:
+            raise ValueError(f"max_tokens={int(max_tokens)} is below the longest unit's {actual} tokens")
+        return int(max_tokens)
+
     def _check_q(self, q) -> torch.Tensor:
         c = self.cache
         self._sync()
@@ -550,7 +561,7 @@ class UnitView:
         c = self.cache
         q = self._check_q(q)
         G = q.shape[1]
-        T_max = int(max_tokens if max_tokens is not None else self.max_tokens)
+        T_max = self._t_max(max_tokens)
         if T_max <= 0:
             raise ValueError("cannot attend over an empty cache")
         if out is None:
@@ -571,7 +582,7 @@ class UnitView:
         c = self.cache
         q = self._check_q(q)
         G = q.shape[1]
-        T_max = int(max_tokens if max_tokens is not None else self.max_tokens)
+        T_max = self._t_max(max_tokens)
         if T_max <= 0:
             raise ValueError("cannot attend over an empty cache")
         ws = self.workspace(G, T_max)
@@ -584,7 +595,7 @@ class UnitView:
         c = self.cache
         q = self._check_q(q)
         G = q.shape[1]
-        T_max = int(max_tokens if max_tokens is not None else self.max_tokens)
+        T_max = self._t_max(max_tokens)
         if out is not None:
             if (out.dtype != torch.float32 or out.dim() != 3 or tuple(out.shape[:2]) != (self.n_units, G)
                     or out.shape[2] < T_max or out.stride(2) != 1 or out.stride(1) != out.shape[2]

@@ -150,6 +150,11 @@ def test_scores_into_caller_buffer():
         view.scores(q, max_tokens=T, out=torch.empty((G, U, T), device="cuda").transpose(0, 1))
     with pytest.raises(ValueError):
         view.scores(q, max_tokens=T, out=buf[:, :, : T - 1])
+    # a tile bound below the longest unit would cut its tokens (and overrun score rows)
+    with pytest.raises(ValueError, match="max_tokens"):
+        view.scores(q, max_tokens=T - 1)
+    with pytest.raises(ValueError, match="max_tokens"):
+        view.decode(q, max_tokens=T - 64)
 
 
 @pytest.mark.parametrize("T,res", [(32768, 0), (9000, 64), (33, 32), (1, 1), (65, 0)])
