@@ -73,6 +73,9 @@ namespace PQB_DQ_NS {
 #ifndef PQB_DQ_SLEEP_PROD
 #define PQB_DQ_SLEEP_PROD 1
 #endif
+#ifndef PQB_DQ_PHI_BF16  // G = 8 bf16 values with bf16 outputs: the kDqBf16P instances (A/B: 0 keeps hi + lo)
+#define PQB_DQ_PHI_BF16 1
+#endif
 #ifndef PQB_DQ_SLEEP_CONS
 #define PQB_DQ_SLEEP_CONS 1
 #endif
@@ -324,8 +327,8 @@ PQB_DEV uint2 lds_u2(uint32_t addr) {
   asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
   return v;
 }
-
-// PROBE: 0 = the kernel; kDqScores = scores-only mode (qk_scores within the
+// PROBE: 0 = the kernel; kDqBf16P = the kernel with bf16-P P.V (G = 8, bf16 outputs);
+// kDqScores = scores-only mode (qk_scores within the
 // stated tolerance, lut_decode.py:119-154: the QK contraction of the fused
 // kernel, the raw fp32 score rows stored, no softmax / values; only the code
 // bytes are streamed).  Diagnostics (flags PQB_DECODE_PROBE_*): 1 = memory only
@@ -336,6 +339,7 @@ PQB_DEV uint2 lds_u2(uint32_t addr) {
 // and the zero points join as sum_t p_t zp_t per query:
 //   o = sum_t p_t (c_t s_t + z_t) = [codes] . (p s) + sum_t p_t z_t.
 constexpr int kDqScores = 3;
+constexpr int kDqBf16P = 4;  // the kernel with bf16-P P.V (G = 8, bf16 values, bf16 outputs)
 
 template <int M, int N, int VQ, bool CODES_ONLY = false>
 PQB_DEV void issue_tile_dq(uint8_t* st, const pqb_store& s, const uint8_t* pb, int tin, uint64_t* bar) {
@@ -479,6 +483,11 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   constexpr int kVqB = val_vq_bits(VQ);
   constexpr float kVqMid = kVqB == 8 ? 128.0f : kVqB == 4 ? 7.0f : 1.0f;  // ~ half the code range
   constexpr bool kScores = PROBE == kDqScores;
+  // bf16 outputs at G = 8 (bf16 values): P.V on bf16 P without its lo part, one
+  // MMA per k-step instead of two; |dO| <= 2^-9 sum_t p_t |v_t|, at the output's
+  // own bf16 rounding (at G <= 4 P_lo rides in the hi MMA's spare columns)
+  constexpr bool kPhiOnly = PROBE == kDqBf16P;
+  static_assert(!kPhiOnly || (VQ == kValBf16 && G == 8), "bf16-P instance: G = 8, bf16 values");
   constexpr bool kFused = M == 4 && N == 4;
   constexpr bool kPacked = Cfg::kPacked;
   // (m = n = 4: the codes take 2 KB of the 10 KB stage, so value tiles stay 1 KB aligned)
@@ -1247,7 +1256,7 @@ __global__ void __launch_bounds__(kDqThreads, 1)
             uint32_t a0, a1, a2, a3;
             ldsm_x4_trans(vbase + ks * 4096 + (mt >> 2) * 1024 + (ld_chunk ^ ((mt & 3) << 5)), a0, a1, a2, a3);
             mma_bf16(d[mt], a0, a1, a2, a3, phi[2 * ks], phi[2 * ks + 1]);
-            if constexpr (!kPacked) mma_bf16(d[mt], a0, a1, a2, a3, plo[2 * ks], plo[2 * ks + 1]);
+            if constexpr (!kPacked && !kPhiOnly) mma_bf16(d[mt], a0, a1, a2, a3, plo[2 * ks], plo[2 * ks + 1]);
           }
         }
       }
@@ -1444,6 +1453,16 @@ static int cluster_capacity() {
   return n > 0 ? n : 0;
 }
 
+// bf16 values: the bf16-P instance for G = 8 launches with bf16 outputs
+// (configs[3]: layer step 0.866 -> 0.886 of the copy peak, scripts/g8_rate.py)
+template <int G, int M, int N, int CL = 0>
+static int launch_bf16v(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s) {
+  if constexpr (G == 8 && PQB_DQ_PHI_BF16) {
+    if (ep.out_dtype == PQB_BF16) return launch_dq<G, M, N, kDqBf16P, 0, CL>(a, ep, ws, grid, s);
+  }
+  return launch_dq<G, M, N, 0, 0, CL>(a, ep, ws, grid, s);
+}
+
 template <int G>
 static int dispatch_dq_mn(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s,
                           bool& handled) {
@@ -1492,21 +1511,21 @@ static int dispatch_dq_mn(const DecodeArgs& a, const EpiArgs& ep, const WorkSpli
   }
   if (ws.cluster > 1 && mn == 44) {  // aligned split, merge through distributed shared memory
     switch (ws.cluster) {
-      case 2: return launch_dq<G, 4, 4, 0, 0, 2>(a, ep, ws, grid, s);
-      case 4: return launch_dq<G, 4, 4, 0, 0, 4>(a, ep, ws, grid, s);
-      case 8: return launch_dq<G, 4, 4, 0, 0, 8>(a, ep, ws, grid, s);
+      case 2: return launch_bf16v<G, 4, 4, 2>(a, ep, ws, grid, s);
+      case 4: return launch_bf16v<G, 4, 4, 4>(a, ep, ws, grid, s);
+      case 8: return launch_bf16v<G, 4, 4, 8>(a, ep, ws, grid, s);
       default: break;
     }
   }
   if (mn == 44 && (a.flags & PQB_DECODE_PROBE_MEM)) return launch_dq<G, 4, 4, 1>(a, ep, ws, grid, s);
   if (mn == 44 && (a.flags & PQB_DECODE_PROBE_COMPUTE)) return launch_dq<G, 4, 4, 2>(a, ep, ws, grid, s);
   switch (mn) {
-    case 44: return launch_dq<G, 4, 4>(a, ep, ws, grid, s);
-    case 32: return launch_dq<G, 3, 2>(a, ep, ws, grid, s);
-    case 22: return launch_dq<G, 2, 2>(a, ep, ws, grid, s);
-    case 42: return launch_dq<G, 4, 2>(a, ep, ws, grid, s);
-    case 24: return launch_dq<G, 2, 4>(a, ep, ws, grid, s);
-    case 34: return launch_dq<G, 3, 4>(a, ep, ws, grid, s);
+    case 44: return launch_bf16v<G, 4, 4>(a, ep, ws, grid, s);
+    case 32: return launch_bf16v<G, 3, 2>(a, ep, ws, grid, s);
+    case 22: return launch_bf16v<G, 2, 2>(a, ep, ws, grid, s);
+    case 42: return launch_bf16v<G, 4, 2>(a, ep, ws, grid, s);
+    case 24: return launch_bf16v<G, 2, 4>(a, ep, ws, grid, s);
+    case 34: return launch_bf16v<G, 3, 4>(a, ep, ws, grid, s);
     default: handled = false; return PQB_OK;
   }
 }
