@@ -76,6 +76,10 @@ namespace PQB_DQ_NS {
 #ifndef PQB_DQ_PHI_BF16  // G = 8 bf16 values with bf16 outputs: the kDqBf16P instances (A/B: 0 keeps hi + lo)
 #define PQB_DQ_PHI_BF16 1
 #endif
+#ifndef PQB_DQ_PHI_BF16_G4  // the same at G = 4: P_lo is free in the MMA there, but its computation and
+                            // packing shuffles are not (configs[1] +1.5 %, scripts/gpu_g4phi_ab.sh)
+#define PQB_DQ_PHI_BF16_G4 1
+#endif
 #ifndef PQB_DQ_SLEEP_CONS
 #define PQB_DQ_SLEEP_CONS 1
 #endif
@@ -327,7 +331,7 @@ PQB_DEV uint2 lds_u2(uint32_t addr) {
   asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
   return v;
 }
-// PROBE: 0 = the kernel; kDqBf16P = the kernel with bf16-P P.V (G = 8, bf16 outputs);
+// PROBE: 0 = the kernel; kDqBf16P = the kernel with bf16-P P.V (G = 4 / 8, bf16 outputs);
 // kDqScores = scores-only mode (qk_scores within the
 // stated tolerance, lut_decode.py:119-154: the QK contraction of the fused
 // kernel, the raw fp32 score rows stored, no softmax / values; only the code
@@ -339,7 +343,7 @@ PQB_DEV uint2 lds_u2(uint32_t addr) {
 // and the zero points join as sum_t p_t zp_t per query:
 //   o = sum_t p_t (c_t s_t + z_t) = [codes] . (p s) + sum_t p_t z_t.
 constexpr int kDqScores = 3;
-constexpr int kDqBf16P = 4;  // the kernel with bf16-P P.V (G = 8, bf16 values, bf16 outputs)
+constexpr int kDqBf16P = 4;  // the kernel with bf16-P P.V (G = 4 / 8, bf16 values, bf16 outputs)
 
 template <int M, int N, int VQ, bool CODES_ONLY = false>
 PQB_DEV void issue_tile_dq(uint8_t* st, const pqb_store& s, const uint8_t* pb, int tin, uint64_t* bar) {
@@ -483,11 +487,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
   constexpr int kVqB = val_vq_bits(VQ);
   constexpr float kVqMid = kVqB == 8 ? 128.0f : kVqB == 4 ? 7.0f : 1.0f;  // ~ half the code range
   constexpr bool kScores = PROBE == kDqScores;
-  // bf16 outputs at G = 8 (bf16 values): P.V on bf16 P without its lo part, one
-  // MMA per k-step instead of two; |dO| <= 2^-9 sum_t p_t |v_t|, at the output's
-  // own bf16 rounding (at G <= 4 P_lo rides in the hi MMA's spare columns)
+  // bf16 outputs (bf16 values): P.V on bf16 P without its lo part -- at G = 8 one
+  // MMA per k-step instead of two, at G = 4 (P_lo rides in the hi MMA's spare
+  // columns) no P_lo conversion and packing shuffles; |dO| <= 2^-9 sum_t p_t |v_t|,
+  // at the output's own bf16 rounding
   constexpr bool kPhiOnly = PROBE == kDqBf16P;
-  static_assert(!kPhiOnly || (VQ == kValBf16 && G == 8), "bf16-P instance: G = 8, bf16 values");
+  static_assert(!kPhiOnly || (VQ == kValBf16 && (G == 8 || G == 4)), "bf16-P instance: G = 4 / 8, bf16 values");
   constexpr bool kFused = M == 4 && N == 4;
   constexpr bool kPacked = Cfg::kPacked;
   // (m = n = 4: the codes take 2 KB of the 10 KB stage, so value tiles stay 1 KB aligned)
@@ -1164,10 +1169,12 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           p1 *= zsv.w;
         }
         const __nv_bfloat162 hi = __floats2bfloat162_rn(p0, p1);
-        const float2 hf = __bfloat1622float2(hi);
-        const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
         phi[nb] = *reinterpret_cast<const uint32_t*>(&hi);
-        plo[nb] = *reinterpret_cast<const uint32_t*>(&lo);
+        if constexpr (!kPhiOnly) {
+          const float2 hf = __bfloat1622float2(hi);
+          const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+          plo[nb] = *reinterpret_cast<const uint32_t*>(&lo);
+        }
       }
       l_run = fmaf(l_run, alpha, ls);
       if constexpr (kVq4) z_run = fmaf(z_run, alpha, zs);
@@ -1181,7 +1188,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
           d[mt][3] *= a1;
         }
       }
-      if constexpr (kPacked) {  // columns 4..7 (lanes 16..31) take P_lo of query g8 - 4
+      if constexpr (kPacked && kPhiOnly) {  // columns 4..7 (lanes 16..31) stay zero
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) phi[nb] = lane < 16 ? phi[nb] : 0u;
+      } else if constexpr (kPacked) {  // columns 4..7 (lanes 16..31) take P_lo of query g8 - 4
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb) {
           const uint32_t o = __shfl_xor_sync(0xffffffffu, plo[nb], 16);
@@ -1453,11 +1463,12 @@ static int cluster_capacity() {
   return n > 0 ? n : 0;
 }
 
-// bf16 values: the bf16-P instance for G = 8 launches with bf16 outputs
-// (configs[3]: layer step 0.866 -> 0.886 of the copy peak, scripts/g8_rate.py)
+// bf16 values: the bf16-P instance for G = 4 / 8 launches with bf16 outputs
+// (configs[3]: layer step 0.866 -> 0.886 of the copy peak, scripts/g8_rate.py;
+// configs[1]: +1.5 % value and sustained at the power cap, scripts/gpu_g4phi_ab.sh)
 template <int G, int M, int N, int CL = 0>
 static int launch_bf16v(const DecodeArgs& a, const EpiArgs& ep, const WorkSplit& ws, int grid, cudaStream_t s) {
-  if constexpr (G == 8 && PQB_DQ_PHI_BF16) {
+  if constexpr ((G == 8 || (G == 4 && PQB_DQ_PHI_BF16_G4)) && PQB_DQ_PHI_BF16) {
     if (ep.out_dtype == PQB_BF16) return launch_dq<G, M, N, kDqBf16P, 0, CL>(a, ep, ws, grid, s);
   }
   return launch_dq<G, M, N, 0, 0, CL>(a, ep, ws, grid, s);
