@@ -80,6 +80,10 @@ namespace PQB_DQ_NS {
                             // packing shuffles are not (configs[1] +1.5 %, scripts/gpu_g4phi_ab.sh)
 #define PQB_DQ_PHI_BF16_G4 1
 #endif
+#ifndef PQB_DQ_FULL_TILE  // softmax of a tile wholly inside the sequence without per-token bound tests
+                          // (configs[1] sustained +0.8 %, value unchanged: scripts/gpu_bench_ab.sh)
+#define PQB_DQ_FULL_TILE 1
+#endif
 #ifndef PQB_DQ_SLEEP_CONS
 #define PQB_DQ_SLEEP_CONS 1
 #endif
@@ -1095,13 +1099,23 @@ __global__ void __launch_bounds__(kDqThreads, 1)
       }
       // ---- online softmax (query g8; the four t4 lanes share it)
       float mx = -INFINITY;
+      if (PQB_DQ_FULL_TILE && tok0 + kTile <= T) {  // whole tile inside the sequence: no bound tests
 #pragma unroll
-      for (int nb = 0; nb < 4; ++nb)
+        for (int nb = 0; nb < 4; ++nb)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          x[nb][j] = tok0 + 8 * nb + 2 * t4 + j < T ? x[nb][j] * xscale : -INFINITY;
-          mx = fmaxf(mx, x[nb][j]);
-        }
+          for (int j = 0; j < 2; ++j) {
+            x[nb][j] *= xscale;
+            mx = fmaxf(mx, x[nb][j]);
+          }
+      } else {
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            x[nb][j] = tok0 + 8 * nb + 2 * t4 + j < T ? x[nb][j] * xscale : -INFINITY;
+            mx = fmaxf(mx, x[nb][j]);
+          }
+      }
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
       const float mn = fmaxf(m_run, mx);
