@@ -84,6 +84,11 @@ namespace PQB_DQ_NS {
                           // (configs[1] sustained +0.8 %, value unchanged: scripts/gpu_bench_ab.sh)
 #define PQB_DQ_FULL_TILE 1
 #endif
+#ifndef PQB_DQ_TWO_CHAINS  // two MMA accumulation chains per n-block in the QK block (m4n4, bf16 values);
+                           // with the bf16-P instances one chain measures better (configs[3] 0.886 -> 0.897,
+                           // configs[1] value +1 %, sustained equal: scripts/gpu_abcd.sh)
+#define PQB_DQ_TWO_CHAINS 0
+#endif
 #ifndef PQB_DQ_SLEEP_CONS
 #define PQB_DQ_SLEEP_CONS 1
 #endif
@@ -803,9 +808,10 @@ __global__ void __launch_bounds__(kDqThreads, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k) sc[nb][k] = sc2[nb][k] = 0.0f;
         }
-        // m = n = 4 with bf16 values: two chains per n-block (A/B +1% G = 4, +3% G = 8);
-        // the other instances measured better with one (m3n2 -6%, 4-bit values -1.5%)
-        constexpr bool kTwoChains = kFused && !kVq4;
+        // m = n = 4 with bf16 values: two chains per n-block measured +1% G = 4, +3% G = 8
+        // before the bf16-P instances and worse since (PQB_DQ_TWO_CHAINS, off); the other
+        // instances always measured better with one (m3n2 -6%, 4-bit values -1.5%)
+        constexpr bool kTwoChains = PQB_DQ_TWO_CHAINS && kFused && !kVq4;
 #pragma unroll
         for (int ks = 0; ks < 16; ks += 2) {
 #pragma unroll
