@@ -232,19 +232,35 @@ class PeerGather:
         handles = [None] * plan.world
         dist.all_gather_object(handles, mine, group=group)
         self.peer_out, self.peer_flags = [], []  # raw base pointers on this device
-        for r, (ho, hf) in enumerate(handles):
-            if r == plan.rank:
-                self.peer_out.append(self._own[0])
-                self.peer_flags.append(self._own[1])
-                continue
-            ptrs = []
-            for h in (ho, hf):
-                p = ctypes.c_void_p()
-                _lib.call("pqb_ipc_open", self.dev, ctypes.create_string_buffer(h, len(h)), ctypes.byref(p))
-                self._opened.append(p.value)
-                ptrs.append(p.value)
-            self.peer_out.append(ptrs[0])
-            self.peer_flags.append(ptrs[1])
+        err = ""
+        try:
+            for r, (ho, hf) in enumerate(handles):
+                if r == plan.rank:
+                    self.peer_out.append(self._own[0])
+                    self.peer_flags.append(self._own[1])
+                    continue
+                ptrs = []
+                for h in (ho, hf):
+                    p = ctypes.c_void_p()
+                    _lib.call("pqb_ipc_open", self.dev, ctypes.create_string_buffer(h, len(h)), ctypes.byref(p))
+                    self._opened.append(p.value)
+                    ptrs.append(p.value)
+                self.peer_out.append(ptrs[0])
+                self.peer_flags.append(ptrs[1])
+        except (RuntimeError, ValueError) as exc:
+            err = str(exc)
+        # every rank must have mapped every peer, or none uses the fused gather
+        errs = [None] * plan.world
+        dist.all_gather_object(errs, err, group=group)
+        if any(errs):
+            for p in self._opened:
+                _lib.load().pqb_ipc_close(self.dev, p)
+            dist.barrier(group=group)  # every importer has unmapped before the owners free
+            self.out = self.flags = None
+            for p in self._own:
+                _lib.load().pqb_ipc_free(self.dev, p)
+            self._opened, self._own = [], []
+            raise RuntimeError(f"peer gather: mapping the peers' buffers failed: {[e for e in errs if e][0]}")
         self._desc = [[self._descriptor(p, layer) for layer in range(S.layers)] for p in range(2)]
 
     def close(self) -> None:
